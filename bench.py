@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of one MC-PDIPM SCM iteration (build + Cholesky) on B200.
+
+BASELINE.json metric: "SCM build+Cholesky s/iter, B-entries/s, % HBM/FP64 roofline at 1/2/4/8 B200".
+One step = sdpc_factor_xinv (a1) + sdpc_scm_build ((a2) chol(Y), (b) solves, (c) accumulate)
++ sdpc_scm_cholesky (d) on fixed seeded synthetic inputs.  value = B-entries/s
+= m(m+1)/2 / (s/iter), summed over ranks.  Default workload: configs[1] (max-cut on the 100x100
+torus, n = m = 10,000), the configuration the metric is quoted on that fits one GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py executes it) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SCM build+Cholesky s/iter, B-entries/s, % HBM/FP64 roofline at 1/2/4/8 B200"
+CONFIG_TEXT = {
+    0: "configs[0]: max-cut SDP, 10x10 torus, n=m=100, MD order",
+    1: "configs[1]: spin-glass max-cut SDP, 100x100 torus, n=m=10000, ND order",
+    2: "configs[2]: theta max-clique SDP, 60x60 torus, n=3600, m=7201, MD order",
+    3: "configs[3]: block-arrow SDP, n=20200, m=5000, identity order",
+    4: "configs[4]: max-cut SDP, 200x200 torus, n=m=40000, ND order",
+}
+# Nominal B200 ratio FP64-tensor / BF16-dense (45 / 2250 TFLOP/s, /opt/skills guides) applied to the
+# measured bf16 peak (MEASURED_PEAKS.json) -> FP64 tensor peak for the roofline.
+FP64_OVER_BF16 = 45.0 / 2250.0
+FALLBACK_BF16 = dict(burst=1590.0, sustained=1400.0)   # B200_PROFILING.md fallback
+FALLBACK_HBM = 6650.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return dict(bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    hbm=d["hbm_gbs"], src="measured (MEASURED_PEAKS.json)")
+    except Exception:
+        return dict(bf16=FALLBACK_BF16["burst"], bf16_sus=FALLBACK_BF16["sustained"], hbm=FALLBACK_HBM,
+                    src="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def entries(m):
+    return m * (m + 1) / 2.0
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import __graft_entry__
+    from instances import gen_config
+
+    __graft_entry__.build()
+    from paper_1310_6919_b200 import Handle, fp64_peak
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    inst = gen_config(args.config, seed=args.seed)
+    n, m = inst.n, inst.m
+    h = Handle.from_instance(inst, device=local_rank)
+    st = h.get_structure()
+    assert np.array_equal(st["rowind"], inst.rowind), "library E differs from the generator's E"
+    x = torch.from_numpy(inst.xbar).to(dev)
+    y = torch.from_numpy(inst.y).to(dev)
+    ld = m + (m & 1)
+    Bt = torch.empty((m, ld), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)   # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        h.factor_xinv(x, stream)
+        h.scm_build(y, Bt, ld, stream)
+        info = h.scm_cholesky(Bt, ld, stream)
+        assert info == 0
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = h.launch_count()
+    times, phases = [], []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)                      # L2 flush between timed iterations (not timed)
+            ev0.record(stream)
+            step()
+            ev1.record(stream)
+            ev1.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            phases.append(h.phase_times())
+    torch.cuda.synchronize()
+    launches = h.launch_count() - l0
+    ms = statistics.mean(times)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+
+    # end to end through the public host-buffer API (H2D inputs + D2H diag(R), info)
+    rd = np.zeros(m)
+    h.iteration_host(inst.xbar, inst.y, rd)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(2, min(args.steps, 5))):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        info = h.iteration_host(inst.xbar, inst.y, rd)
+        e2e_t.append((time.perf_counter() - t0) * 1e3)
+        assert info == 0
+    e2e_ms = statistics.mean(e2e_t)
+
+    if rank != 0:
+        return None
+    pk = peaks()
+    ph = [statistics.mean(p[i] for p in phases) for i in range(8)]
+    upd_ms, n_upd, upd_flops = ph[5], ph[6], ph[7]
+    fp64_peak_tf = pk["bf16_sus"] * FP64_OVER_BF16
+    achieved = upd_flops / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else None
+    dmma = dfma = None
+    if args.measure_peak:
+        dmma, dfma = fp64_peak(local_rank, 1500.0)
+    value = world * entries(m) / (ms * 1e-3)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "B-entries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "s_per_iter": ms * 1e-3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, instances/; SURVEY.md §8(d) recipe)",
+        "config": {"workload": CONFIG_TEXT[args.config], "n": n, "m": m, "nnzE": int(inst.nnzE), "seed": args.seed,
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "l2": "256 MB buffer written between timed steps (L2 flush); step working set ~2.4 GB"},
+        "phases_ms": {"a1_factor_xinv": ph[0], "a2_chol_y": ph[1], "b_solves": ph[2], "c_accumulate": ph[3],
+                      "d_cholesky": ph[4], "d_trailing_updates": upd_ms},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "roofline": {"kernel": "gemm_nt_kernel<SYRK> (SCM Cholesky trailing update, DMMA)",
+                     "bound": "tensor", "achieved": achieved, "peak": fp64_peak_tf, "unit": "TFLOP/s",
+                     "frac": (achieved / fp64_peak_tf) if achieved else None, "traffic": None,
+                     "peak_source": f"{pk['src']} bf16 sustained {pk['bf16_sus']} x FP64/BF16 nominal 45/2250",
+                     "launches_per_step": n_upd, "flops_per_step": upd_flops,
+                     "fp64_microbench_tflops": {"dmma": dmma, "dfma": dfma}},
+        "e2e": {"value": world * entries(m) / (e2e_ms * 1e-3), "unit": "B-entries/s",
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(2 * 8 * inst.nnzE),
+                "d2h_bytes_per_step": int(8 * m + 4),
+                "api": "sdpc_iteration_host (host xbar_E, y_E in; diag(R), info out)"},
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(inst, args)
+    return line
+
+
+# ----------------------------------------------------------------------------- oracle (reference arm)
+
+def cpu_baseline(inst, args, budget_cols=None):
+    """Time the oracle as it stands on a bounded sample; extrapolate to one full iteration."""
+    import numpy as np
+
+    from oracle import algorithm1 as A1, cholesky as CH, scm as SCM, symbolic as SYM
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    S = SYM.analyse(inst.n, inst.perm, inst.a_row, inst.a_col)
+    t_sym = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    L, D = A1.factor_xinv(S, inst.xbar)
+    t_a1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    solver = SCM.ColumnSolver(S, L, D, inst.y, inst.perm)
+    t_fac = time.perf_counter() - t0
+    ncols = budget_cols or min(inst.m, 64)
+    cols = list(range(0, inst.m, max(1, inst.m // ncols)))[:ncols]
+    t0 = time.perf_counter()
+    SCM.scm_columns(inst, cols, solver)
+    t_cols = time.perf_counter() - t0
+    msub = min(inst.m, 4000)
+    rng = np.random.default_rng(0)
+    G = rng.standard_normal((msub, msub))
+    Bs = G @ G.T + msub * np.eye(msub)
+    t0 = time.perf_counter()
+    CH.potrf_lower(Bs)
+    t_chol = time.perf_counter() - t0
+    m = inst.m
+    t_iter = t_a1 + t_fac + t_cols * (m / len(cols)) + t_chol * (m / msub) ** 3
+    return {"value": entries(m) / t_iter, "unit": "B-entries/s", "s_per_iter": t_iter, "cores": cores,
+            "kind": "oracle",
+            "sample": (f"oracle Algorithm 1 on all cliques ({t_a1:.2f} s) + Y factorization ({t_fac:.2f} s) + "
+                       f"{len(cols)} of {m} SCM columns by sparse solves ({t_cols:.2f} s, x{m / len(cols):.0f}) + "
+                       f"LAPACK potrf of a {msub}x{msub} SPD matrix ({t_chol:.2f} s, x(m/{msub})^3); "
+                       f"extrapolated to one iteration; symbolic setup {t_sym:.2f} s excluded")}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from instances import gen_config
+    inst = gen_config(args.config, seed=args.seed)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(inst, args, budget_cols=16)
+        if i >= args.warmup:
+            vals.append(cb)
+    ms = statistics.mean(v["s_per_iter"] for v in vals) * 1e3
+    value = entries(inst.m) / (ms * 1e-3)
+    last = vals[-1]
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "B-entries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[args.config], "n": inst.n, "m": inst.m, "seed": args.seed},
+            "cpu_baseline": {"value": value, "unit": "B-entries/s", "cores": last["cores"], "kind": "oracle",
+                             "sample": last["sample"]},
+            "e2e": {"value": value, "unit": "B-entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--measure-peak", action="store_true", default=True)
+    ap.add_argument("--no-measure-peak", dest="measure_peak", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1 and args.impl == "ours":
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

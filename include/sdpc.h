@@ -1,0 +1,183 @@
+/*
+ * sdpc.h - C ABI of libsdpc, the B200-native Schur-complement (SCM) engine for the
+ * matrix-completion primal-dual interior-point method (MC-PDIPM) of
+ * Yamashita & Nakata, arXiv 1310.6919 (PAPER.md, cited as P:<line>).
+ *
+ * One PDIPM iteration's hot path is three calls:
+ *   sdpc_factor_xinv   (a1)  Algorithm 1: X-hat^{-1} = L D L^T from the partial X-bar on E
+ *                            (Alg. 1; L-hat = L D^{1/2}).
+ *   sdpc_scm_build     (a2)  Y = L_Y D_Y L_Y^T on E (type (v)),
+ *                      (b)   x_p = X-hat e_p, y_q = Y^{-1} e_q by multi-RHS supernodal solves
+ *                            (P:686-688 Eq. newSCM2, Alg. 2 Step 3-3),
+ *                      (c)   B_kl = sum_{(p,q) in A_l} [A_l]_pq x_p^T A_k y_q  for k >= l
+ *                            (P:380 Eq. SCM; lower triangle only).
+ *   sdpc_scm_cholesky  (d)   dense B = R R^T in FP64 (type (i)).
+ *
+ * Conventions for every entry point:
+ *   - 0-based indices.  "E" is the extended sparsity pattern as a lower CSC
+ *     in ELIMINATION order: column j holds row j first, then struct(L_{*j}) ascending.
+ *   - Host arrays passed in are COPIED; the caller keeps ownership.  Device pointers
+ *     (xbar_E, y_E, B, L_E, D, ...) are owned by the caller (e.g. torch tensors) and
+ *     must stay valid until the call returns.  The handle owns its factors,
+ *     structure and workspaces and frees them in sdpc_destroy.
+ *   - Calls enqueue on `stream` (a cudaStream_t passed as void*; NULL = legacy default)
+ *     and RETURN AFTER THE STREAM WORK COMPLETED, so status and info are exact.
+ *   - No exceptions or exit() cross the ABI.  Errors are status codes; the index
+ *     of a failing pivot / clique is available through sdpc_last_info().
+ *   - One handle per rank (GPU); calls on one handle must be serialised by the caller.
+ *   - There is no CPU fallback: without a usable sm_100 device sdpc_create fails
+ *     with SDPC_ERR_CUDA.
+ */
+#ifndef SDPC_H
+#define SDPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SDPC_OK = 0,
+  SDPC_ERR_INVALID_ARG = 1,  /* bad size/pointer/pattern (e.g. perm not a permutation)           */
+  SDPC_ERR_NOT_PD = 2,       /* a clique block, Y, or B is not positive definite; see last_info  */
+  SDPC_ERR_OOM = 3,          /* device or host allocation failed                                 */
+  SDPC_ERR_CUDA = 4,         /* CUDA runtime error, or no sm_100 device                          */
+  SDPC_ERR_NCCL = 5,         /* NCCL failure (multi-GPU)                                         */
+  SDPC_ERR_STATE = 6         /* call order violated (e.g. scm_build before factor_xinv)          */
+} sdpc_status;
+
+typedef struct sdpc_ctx* sdpc_handle;
+
+/* Host views into the handle's symbolic structure (valid until sdpc_destroy). */
+typedef struct {
+  int32_t n;             /* order of X and Y                                                   */
+  int32_t m;             /* number of constraints A_1..A_m                                      */
+  int64_t nnzE;          /* |E| lower incl. diagonal                                            */
+  const int32_t* perm;   /* [n] perm[new] = old (elimination order)                            */
+  const int32_t* parent; /* [n] elimination-tree parent (new ids), -1 at roots                 */
+  const int64_t* colptr; /* [n+1] CSC column pointers of E                                     */
+  const int32_t* rowind; /* [nnzE] row indices, ascending, diagonal first in each column        */
+  int32_t nsuper;        /* number of fundamental supernodes = cliques C_r of Algorithm 1      */
+  const int32_t* super_ptr; /* [nsuper+1] first column of each supernode (S_r = [sp[r], sp[r+1])) */
+} sdpc_structure;
+
+/* 2D block-cyclic layout of B on this rank (1x1 grid when nranks == 1). */
+typedef struct {
+  int32_t nb;            /* tile size                                                          */
+  int32_t Pr, Pc;        /* process grid                                                       */
+  int32_t myrow, mycol;  /* this rank's grid coordinates                                       */
+  int64_t mloc, nloc;    /* local rows / columns of B held by this rank                        */
+  int64_t lld;           /* required minimum leading dimension of the local buffer             */
+} sdpc_layout;
+
+/*
+ * sdpc_create - set up the problem (P): min A_0.X s.t. A_k.X = b_k (k = 1..m), X >= 0
+ * (P:83-106), and run the one-time symbolic analysis:
+ * aggregate pattern, elimination order, E, elimination tree,
+ * fundamental supernodes used as the cliques C_r / S_r, solve schedules.
+ *
+ *   n, m        : order and number of constraints (n >= 1, m >= 1).
+ *   a_ptr[m+2]  : entries of A_k are [a_ptr[k], a_ptr[k+1]) for k = 0..m (A_0 = objective).
+ *   a_row, a_col, a_val : lower triplets, ORIGINAL ids, row >= col; [A_k]_ij = [A_k]_ji = val.
+ *                 Duplicates within one A_k are summed.
+ *   b[m]        : right-hand side; validated finite, does not enter B.
+ *   perm[n]     : elimination order, perm[new] = old; NULL => built-in exact minimum degree
+ *                 (ties -> smallest original id).
+ *   device      : CUDA device ordinal this handle runs on.
+ *   nranks, rank, nccl_id : multi-GPU world (nranks == 1: rank 0, nccl_id NULL).
+ * Host arrays are copied.  Errors: INVALID_ARG (sizes, out-of-range ids, row < col,
+ * perm not a permutation), OOM, CUDA (no device / not sm_100), NCCL.
+ */
+sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m,
+                        const int64_t* a_ptr, const int32_t* a_row, const int32_t* a_col,
+                        const double* a_val, const double* b, const int32_t* perm,
+                        int32_t device, int32_t nranks, int32_t rank, const void* nccl_id);
+
+/* 128-byte ncclUniqueId for multi-GPU handles (rank 0 creates, the caller broadcasts). */
+sdpc_status sdpc_get_unique_id(void* id_out /* 128 bytes */);
+
+sdpc_status sdpc_get_structure(sdpc_handle h, sdpc_structure* out);
+sdpc_status sdpc_get_scm_layout(sdpc_handle h, sdpc_layout* out);
+
+/*
+ * sdpc_factor_xinv - (a1) Algorithm 1: for every clique r, reverse-permute
+ * X-bar_{C_r C_r} (Step 2-1), Cholesky it (Step 2-2), form L_r = P_r M_r^{-T} P_r (Step 2-3)
+ * and keep its first |S_r| columns (Step 3).  Kept on device in the handle as unit-lower
+ * L and diagonal D with L-hat = L D^{1/2}, X-hat^{-1} = L D L^T (SURVEY §8(c) reading #1).
+ *   xbar_E : DEVICE [nnzE] fp64, X-bar on E in E's CSC order (sdpc_get_structure).
+ * Errors: NOT_PD with sdpc_last_info() = clique index r (0-based) whose block failed.
+ */
+sdpc_status sdpc_factor_xinv(sdpc_handle h, const double* xbar_E, void* stream);
+
+/* Copy the (a1) factor out: L_E DEVICE [nnzE] (unit diagonal stored), D DEVICE [n]. */
+sdpc_status sdpc_get_xinv_factor(sdpc_handle h, double* L_E, double* D, void* stream);
+
+/*
+ * sdpc_scm_build - (a2)+(b)+(c).  Factors Y = L_Y D_Y L_Y^T on E (NOT_PD: last_info =
+ * elimination column j), evaluates x_p = X-hat e_p and y_q = Y^{-1} e_q for the needed
+ * columns, and writes B_kl = (X-hat A_k Y^{-1}) . A_l for k >= l into the lower triangle of
+ * the column-major B (constraint order as given; k, l = 0..m-1 <-> A_1..A_m).
+ * The strict upper triangle of B is not referenced.
+ *   y_E : DEVICE [nnzE] fp64, Y on E in E's CSC order.
+ *   B   : DEVICE, m x m column-major with leading dimension ldb >= m (nranks == 1), or this
+ *         rank's local 2D block-cyclic buffer (sdpc_get_scm_layout) when nranks > 1.
+ * Requires a successful sdpc_factor_xinv on this handle (else STATE).
+ */
+sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t ldb, void* stream);
+
+/* Copy the (a2) factor out: L_Y DEVICE [nnzE], D_Y DEVICE [n] (after sdpc_scm_build). */
+sdpc_status sdpc_get_y_factor(sdpc_handle h, double* LY_E, double* DY, void* stream);
+
+/*
+ * Copy selected columns of X-hat and Y^{-1} computed by the last sdpc_scm_build ((b) output,
+ * for verification).  cols: HOST [ncols] ORIGINAL vertex ids.  X_out, Y_out: DEVICE
+ * n x ncols column-major (ld = n), rows in ORIGINAL order.
+ */
+sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t ncols,
+                                     double* X_out, double* Y_out, void* stream);
+
+/*
+ * sdpc_scm_cholesky - (d) in place: lower(B) <- R with B = R R^T (LAPACK potrf 'L' rule).
+ *   info (HOST): 0 on success; k > 0 if the leading minor of order k is not positive
+ *   definite (pivot <= 0 or NaN), in which case status = NOT_PD and last_info = k.
+ * nranks > 1: B is the local 2D block-cyclic buffer; the factorization is collective.
+ */
+sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream);
+
+/*
+ * sdpc_iteration_host - the whole hot path from HOST buffers (what a host-side PDIPM driver
+ * calls once per iteration): copies xbar_E and y_E (HOST [nnzE]) to the device, runs
+ * factor_xinv -> scm_build -> scm_cholesky into a handle-owned B, and copies back
+ * rdiag (HOST [m], the diagonal of R; NULL allowed) and info (HOST).
+ */
+sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const double* y_E,
+                                double* rdiag, int32_t* info, void* stream);
+
+/* Per-phase device times (ms) of the last calls, from CUDA events on the call's stream:
+ * t[0]=(a1) t[1]=(a2) t[2]=(b) t[3]=(c) t[4]=(d) t[5]=(d) trailing-update kernels only,
+ * t[6]=number of (d) trailing-update launches, t[7]=their total algorithmic flops. */
+sdpc_status sdpc_get_phase_times(sdpc_handle h, double* t /* [8] */);
+
+/* Enable (1) / disable (0) per-phase event timing (default on; costs a few events per call). */
+sdpc_status sdpc_set_timing(sdpc_handle h, int32_t on);
+
+/* Number of kernel launches the handle issued since creation (evidence for gpu_launches). */
+int64_t sdpc_launch_count(sdpc_handle h);
+
+/*
+ * FP64 roof microbenchmarks (N10): sustained DMMA (mma.sync m8n8k4 f64 -> DMMA.8x8x4) and
+ * DFMA throughput over all SMs for about `ms` milliseconds each.  Outputs TFLOP/s.
+ */
+sdpc_status sdpc_fp64_peak(int32_t device, double ms, double* dmma_tflops, double* dfma_tflops);
+
+sdpc_status sdpc_destroy(sdpc_handle h);
+const char* sdpc_status_string(sdpc_status s);
+int64_t sdpc_last_info(sdpc_handle h);
+/* Human-readable detail of the last CUDA/NCCL error seen by the handle ("" if none). */
+const char* sdpc_last_error_message(sdpc_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDPC_H */

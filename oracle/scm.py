@@ -170,21 +170,27 @@ class ColumnSolver:
         return ynew[self.iperm, :]
 
 
-def scm_columns(inst, cols, solver: ColumnSolver):
-    """Full columns B[:, l] (all k) for the constraint indices l in `cols` (0-based)."""
+def scm_columns(inst, cols, solver: ColumnSolver, chunk=128):
+    """Full columns B[:, l] (all k) for the constraint indices l in `cols` (0-based).
+
+    The solves x_p, y_q for all nonzero columns of the sampled A_l are done first, in
+    multi-RHS chunks (same arithmetic as one solve per RHS, Algorithm 2 Step 3-3).
+    """
     m = inst.m
     ents = sym_entries(inst)
     sizes = np.array([e[0].size for e in ents])
     small = np.flatnonzero(sizes <= LARGE)
     large = np.flatnonzero(sizes > LARGE)
     I, J, V = _padded(ents, small)
+    ps = np.unique(np.concatenate([ents[l][0] for l in cols]))
+    qs = np.unique(np.concatenate([ents[l][1] for l in cols]))
+    X = np.concatenate([solver.x(ps[a:a + chunk]) for a in range(0, ps.size, chunk)], axis=1)
+    Yc = np.concatenate([solver.y(qs[a:a + chunk]) for a in range(0, qs.size, chunk)], axis=1)
     out = np.zeros((m, len(cols)))
     for a, l in enumerate(cols):
         p, q, w = ents[l]
-        up, ip = np.unique(p, return_inverse=True)
-        uq, iq = np.unique(q, return_inverse=True)
-        X = solver.x(up)                              # n x |up|
-        Yc = solver.y(uq)
+        ip = np.searchsorted(ps, p)
+        iq = np.searchsorted(qs, q)
         col = np.zeros(m)
         for t in range(p.size):
             xp = X[:, ip[t]]

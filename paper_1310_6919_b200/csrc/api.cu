@@ -1,0 +1,554 @@
+// libsdpc C ABI (include/sdpc.h): handle lifetime, host preprocessing, phase drivers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.hpp"
+#include "sdpc.h"
+
+using namespace sdpc;
+
+namespace {
+
+template <class T>
+cudaError_t upload(T** dst, const std::vector<T>& v) {
+  *dst = nullptr;
+  size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  cudaError_t e = cudaMalloc(dst, bytes);
+  if (e != cudaSuccess) return e;
+  if (!v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+template <class T>
+cudaError_t dalloc(T** dst, size_t count) {
+  *dst = nullptr;
+  return cudaMalloc(dst, std::max<size_t>(1, count) * sizeof(T));
+}
+
+sdpc_status map_cuda(sdpc_ctx* h, cudaError_t e) {
+  if (e == cudaSuccess) return SDPC_OK;
+  if (h) h->err = cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? SDPC_ERR_OOM : SDPC_ERR_CUDA;
+}
+
+#define CK(expr)                                  \
+  do {                                            \
+    cudaError_t _e = (expr);                      \
+    if (_e != cudaSuccess) return map_cuda(h, _e); \
+  } while (0)
+
+constexpr size_t kSmemCap = 220 * 1024;
+
+// size classes for the per-clique kernels
+int class_of(size_t bytes) {
+  if (bytes <= 12 * 1024) return 0;
+  if (bytes <= 48 * 1024) return 1;
+  if (bytes <= kSmemCap) return 2;
+  return 3;
+}
+const int kClassThreads[4] = {64, 128, 256, 512};
+
+cudaError_t build_classes(std::vector<CliqueClass>& cls, const std::vector<int32_t>& members,
+                          const std::vector<size_t>& bytes, const std::vector<int64_t>& ws_off) {
+  cls.assign(4, CliqueClass{});
+  for (int q = 0; q < 4; ++q) cls[q].threads = kClassThreads[q];
+  for (int32_t r : members) {
+    int q = ws_off[r] >= 0 ? 3 : class_of(bytes[r]);
+    cls[q].sn.push_back(r);
+    if (q < 3) cls[q].smem = std::max(cls[q].smem, bytes[r]);
+  }
+  // biggest cliques first so the long CTAs start early
+  for (auto& k : cls) {
+    if (k.sn.empty()) continue;
+    cudaError_t e = upload(&k.d_sn, k.sn);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+void free_classes(std::vector<CliqueClass>& cls) {
+  for (auto& k : cls)
+    if (k.d_sn) cudaFree(k.d_sn);
+  cls.clear();
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float t = 0;
+  if (cudaEventElapsedTime(&t, a, b) != cudaSuccess) return 0;
+  return t;
+}
+
+sdpc_status check_err(sdpc_ctx* h, cudaStream_t st, int32_t* out) {
+  int32_t v = kNoError;
+  CK(cudaMemcpyAsync(&v, h->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  *out = v;
+  return SDPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sdpc_status_string(sdpc_status s) {
+  switch (s) {
+    case SDPC_OK: return "ok";
+    case SDPC_ERR_INVALID_ARG: return "invalid argument";
+    case SDPC_ERR_NOT_PD: return "not positive definite";
+    case SDPC_ERR_OOM: return "out of memory";
+    case SDPC_ERR_CUDA: return "CUDA error";
+    case SDPC_ERR_NCCL: return "NCCL error";
+    case SDPC_ERR_STATE: return "invalid call order";
+  }
+  return "unknown status";
+}
+
+int64_t sdpc_last_info(sdpc_handle h) { return h ? h->last_info : 0; }
+int64_t sdpc_launch_count(sdpc_handle h) { return h ? h->launches : 0; }
+
+const char* sdpc_last_error_message(sdpc_handle h) { return h ? h->err.c_str() : ""; }
+
+sdpc_status sdpc_get_unique_id(void* id_out) {
+  (void)id_out;
+  return SDPC_ERR_NCCL;  // multi-GPU transport not built in this library version
+}
+
+sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a_ptr, const int32_t* a_row,
+                        const int32_t* a_col, const double* a_val, const double* b, const int32_t* perm,
+                        int32_t device, int32_t nranks, int32_t rank, const void* nccl_id) {
+  if (!out) return SDPC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (n < 1 || m < 1 || !a_ptr || !a_val || !b) return SDPC_ERR_INVALID_ARG;
+  if (a_ptr[0] != 0) return SDPC_ERR_INVALID_ARG;
+  for (int32_t k = 0; k <= m; ++k)
+    if (a_ptr[k + 1] < a_ptr[k]) return SDPC_ERR_INVALID_ARG;
+  if (a_ptr[m + 1] > 0 && (!a_row || !a_col)) return SDPC_ERR_INVALID_ARG;
+  for (int32_t k = 0; k < m; ++k)
+    if (!std::isfinite(b[k])) return SDPC_ERR_INVALID_ARG;
+  for (int64_t e = 0; e < a_ptr[m + 1]; ++e)
+    if (!std::isfinite(a_val[e])) return SDPC_ERR_INVALID_ARG;
+  if (nranks != 1 || rank != 0 || nccl_id != nullptr) return SDPC_ERR_INVALID_ARG;  // multi-GPU: not in this build
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SDPC_ERR_CUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return SDPC_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return SDPC_ERR_CUDA;
+
+  sdpc_ctx* h = new (std::nothrow) sdpc_ctx();
+  if (!h) return SDPC_ERR_OOM;
+  h->device = device;
+  Symbolic& S = h->S;
+  std::string msg = analyse(S, n, m, a_ptr, a_row, a_col, perm);
+  if (!msg.empty()) {
+    delete h;
+    return SDPC_ERR_INVALID_ARG;
+  }
+  const int32_t ns = S.nsuper;
+  auto fail = [&](sdpc_status s) {
+    sdpc_destroy(h);
+    return s;
+  };
+
+  // ---- per-clique size classes and global workspace
+  std::vector<size_t> b1(ns), b2(ns);
+  std::vector<int64_t> ws_off(ns, -1);
+  int64_t ws_total = 0;
+  for (int32_t r = 0; r < ns; ++r) {
+    const size_t c = S.snc[r], s = S.sns[r];
+    b1[r] = (c * c + c * s) * sizeof(double);
+    b2[r] = c * c * sizeof(double);
+    if (b1[r] > kSmemCap) {
+      ws_off[r] = ws_total;
+      ws_total += (int64_t)(c * c + c * s);
+    }
+  }
+  std::vector<int32_t> all(ns);
+  for (int32_t r = 0; r < ns; ++r) all[r] = r;
+  std::stable_sort(all.begin(), all.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
+  if (build_classes(h->a1cls, all, b1, ws_off) != cudaSuccess) return fail(SDPC_ERR_OOM);
+  const int nh = (int)S.hlev_ptr.size() - 1;
+  h->a2lev.resize(nh);
+  for (int lv = 0; lv < nh; ++lv) {
+    std::vector<int32_t> mem(S.hlev_sn.begin() + S.hlev_ptr[lv], S.hlev_sn.begin() + S.hlev_ptr[lv + 1]);
+    std::stable_sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
+    if (build_classes(h->a2lev[lv], mem, b2, ws_off) != cudaSuccess) return fail(SDPC_ERR_OOM);
+  }
+
+  // ---- RHS panels: union of the etree paths of each panel's columns (supernode granularity)
+  const int32_t npanels = (n + kPanelW - 1) / kPanelW;
+  std::vector<int32_t> reach_ptr(npanels + 1, 0), reach_sn, stamp(ns, -1), tmp;
+  for (int32_t P = 0; P < npanels; ++P) {
+    tmp.clear();
+    for (int32_t p = P * kPanelW; p < std::min(n, (P + 1) * kPanelW); ++p) {
+      for (int32_t r = S.sn_of_col[p]; r >= 0 && stamp[r] != P; r = S.sparent[r]) {
+        stamp[r] = P;
+        tmp.push_back(r);
+      }
+    }
+    std::sort(tmp.begin(), tmp.end());
+    reach_sn.insert(reach_sn.end(), tmp.begin(), tmp.end());
+    reach_ptr[P + 1] = (int32_t)reach_sn.size();
+  }
+
+  // ---- constraints in elimination ids, symmetric expansion, duplicates summed
+  std::vector<int64_t> cptr(m + 1, 0);
+  std::vector<int32_t> ci, cj;
+  std::vector<double> cv;
+  bool maxcut = true;
+  std::vector<int32_t> vrow(m), col_cons(n, -1);
+  std::vector<double> aval(m);
+  std::vector<uint8_t> is_large(m, 0);
+  std::vector<int32_t> large;
+  for (int32_t k = 0; k < m; ++k) {
+    const int64_t lo = a_ptr[k + 1], hi = a_ptr[k + 2];
+    std::vector<std::pair<std::pair<int32_t, int32_t>, double>> ent;
+    for (int64_t e = lo; e < hi; ++e) ent.push_back({{a_row[e], a_col[e]}, a_val[e]});
+    std::sort(ent.begin(), ent.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    std::vector<std::pair<std::pair<int32_t, int32_t>, double>> merged;
+    for (auto& x : ent) {
+      if (!merged.empty() && merged.back().first == x.first) merged.back().second += x.second;
+      else merged.push_back(x);
+    }
+    for (auto& x : merged) {
+      const int32_t r = S.iperm[x.first.first], c = S.iperm[x.first.second];
+      ci.push_back(r);
+      cj.push_back(c);
+      cv.push_back(x.second);
+      if (r != c) {
+        ci.push_back(c);
+        cj.push_back(r);
+        cv.push_back(x.second);
+      }
+    }
+    cptr[k + 1] = (int64_t)ci.size();
+    const int64_t cnt = cptr[k + 1] - cptr[k];
+    if (cnt > 64) {
+      is_large[k] = 1;
+      large.push_back(k);
+    }
+    if (merged.size() != 1 || merged[0].first.first != merged[0].first.second) {
+      maxcut = false;
+    } else {
+      const int32_t v = S.iperm[merged[0].first.first];
+      if (col_cons[v] >= 0) maxcut = false;
+      else {
+        col_cons[v] = k;
+        vrow[k] = v;
+        aval[k] = merged[0].second;
+      }
+    }
+  }
+
+  // ---- upload
+  DevSym& d = h->d;
+  d.n = n;
+  d.m = m;
+  d.nsuper = ns;
+  d.nnzE = S.nnzE();
+  d.npanels = npanels;
+  cudaError_t e = cudaSuccess;
+#define UP(dst, v)                                    \
+  if ((e = upload(&(dst), (v))) != cudaSuccess) { \
+    h->err = cudaGetErrorString(e);                 \
+    return fail(SDPC_ERR_OOM);                      \
+  }
+  UP(d.colptr, S.colptr);
+  UP(d.rowind, S.rowind);
+  UP(d.super_ptr, S.super_ptr);
+  UP(d.snc, S.snc);
+  UP(d.sns, S.sns);
+  UP(d.sparent, S.sparent);
+  UP(d.panel_off, S.panel_off);
+  UP(d.e2p, S.e2p);
+  UP(d.umap_off, S.umap_off);
+  UP(d.umap, S.umap);
+  UP(d.relind_off, S.relind_off);
+  UP(d.relind, S.relind);
+  UP(d.upd_off, S.upd_off);
+  UP(d.child_ptr, S.child_ptr);
+  UP(d.child_list, S.child_list);
+  UP(d.hlev_sn, S.hlev_sn);
+  UP(d.dlev_ptr, S.dlev_ptr);
+  UP(d.dlev_sn, S.dlev_sn);
+  UP(d.perm, S.perm);
+  UP(d.iperm, S.iperm);
+  UP(d.reach_ptr, reach_ptr);
+  UP(d.reach_sn, reach_sn);
+  UP(h->d_ws_off, ws_off);
+  DevCons& cs = h->cons;
+  cs.maxcut = maxcut;
+  cs.m = m;
+  UP(cs.ptr, cptr);
+  UP(cs.ei, ci);
+  UP(cs.ej, cj);
+  UP(cs.ev, cv);
+  UP(cs.is_large, is_large);
+  UP(cs.large, large);
+  cs.nlarge = (int32_t)large.size();
+  UP(cs.vrow, vrow);
+  UP(cs.aval, aval);
+  UP(cs.col_cons, col_cons);
+#undef UP
+#define AL(dst, cnt)                                    \
+  if ((e = dalloc(&(dst), (cnt))) != cudaSuccess) { \
+    h->err = cudaGetErrorString(e);                   \
+    return fail(SDPC_ERR_OOM);                        \
+  }
+  AL(h->ws, (size_t)ws_total);
+  AL(h->Lx, (size_t)S.panel_total);
+  AL(h->Ly, (size_t)S.panel_total);
+  AL(h->Dx, (size_t)n);
+  AL(h->Dy, (size_t)n);
+  AL(h->upd, (size_t)S.upd_total);
+  AL(h->d_err, 1);
+  AL(h->potrf_ws, 128 * 128);
+#undef AL
+  for (auto& ev : h->ev) cudaEventCreate(&ev);
+  if (cudaGetLastError() != cudaSuccess) return fail(SDPC_ERR_CUDA);
+  *out = h;
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_destroy(sdpc_handle h) {
+  if (!h) return SDPC_OK;
+  cudaSetDevice(h->device);
+  DevSym& d = h->d;
+  void* ptrs[] = {d.colptr, d.rowind, d.super_ptr, d.snc, d.sns, d.sparent, d.panel_off, d.e2p, d.umap_off,
+                  d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
+                  d.dlev_ptr, d.dlev_sn, d.perm, d.iperm, d.reach_ptr, d.reach_sn, h->d_ws_off,
+                  h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
+                  h->cons.vrow, h->cons.aval, h->cons.col_cons, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
+                  h->d_err, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->pinned_in) cudaFreeHost(h->pinned_in);
+  if (h->pinned_out) cudaFreeHost(h->pinned_out);
+  free_classes(h->a1cls);
+  for (auto& lv : h->a2lev) free_classes(lv);
+  for (auto& ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : h->upd_ev) cudaEventDestroy(ev);
+  delete h;
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_get_structure(sdpc_handle h, sdpc_structure* out) {
+  if (!h || !out) return SDPC_ERR_INVALID_ARG;
+  const Symbolic& S = h->S;
+  out->n = S.n;
+  out->m = S.m;
+  out->nnzE = S.nnzE();
+  out->perm = S.perm.data();
+  out->parent = S.parent.data();
+  out->colptr = S.colptr.data();
+  out->rowind = S.rowind.data();
+  out->nsuper = S.nsuper;
+  out->super_ptr = S.super_ptr.data();
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_get_scm_layout(sdpc_handle h, sdpc_layout* out) {
+  if (!h || !out) return SDPC_ERR_INVALID_ARG;
+  out->nb = 128;
+  out->Pr = out->Pc = 1;
+  out->myrow = out->mycol = 0;
+  out->mloc = out->nloc = h->S.m;
+  out->lld = h->S.m;
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_set_timing(sdpc_handle h, int32_t on) {
+  if (!h) return SDPC_ERR_INVALID_ARG;
+  h->timing = on != 0;
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_get_phase_times(sdpc_handle h, double* t) {
+  if (!h || !t) return SDPC_ERR_INVALID_ARG;
+  for (int i = 0; i < 8; ++i) t[i] = h->times[i];
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_factor_xinv(sdpc_handle h, const double* xbar_E, void* stream) {
+  if (!h || !xbar_E) return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  h->have_x = false;
+  h->have_y = false;
+  CK(cudaMemsetAsync(h->d_err, 0x7f, sizeof(int32_t), st));
+  if (h->timing) CK(cudaEventRecord(h->ev[0], st));
+  h->launches += launch_alg1(h, xbar_E, st);
+  if (h->timing) CK(cudaEventRecord(h->ev[1], st));
+  int32_t v;
+  sdpc_status s = check_err(h, st, &v);
+  if (s != SDPC_OK) return s;
+  if (h->timing) h->times[0] = elapsed(h->ev[0], h->ev[1]);
+  if (v != kNoError) {
+    h->last_info = v;
+    return SDPC_ERR_NOT_PD;
+  }
+  h->have_x = true;
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_get_xinv_factor(sdpc_handle h, double* L_E, double* D, void* stream) {
+  if (!h || !L_E || !D) return SDPC_ERR_INVALID_ARG;
+  if (!h->have_x) return SDPC_ERR_STATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  h->launches += launch_panels_to_E(h, h->Lx, L_E, st);
+  CK(cudaMemcpyAsync(D, h->Dx, sizeof(double) * h->S.n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_get_y_factor(sdpc_handle h, double* LY_E, double* DY, void* stream) {
+  if (!h || !LY_E || !DY) return SDPC_ERR_INVALID_ARG;
+  if (!h->have_y) return SDPC_ERR_STATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  h->launches += launch_panels_to_E(h, h->Ly, LY_E, st);
+  CK(cudaMemcpyAsync(DY, h->Dy, sizeof(double) * h->S.n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t ldb, void* stream) {
+  if (!h || !y_E || !B || ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
+  if (!h->have_x) return SDPC_ERR_STATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  h->have_y = false;
+  const size_t dense = (size_t)h->d.npanels * h->S.n * kPanelW;
+  if (!h->Xh) {
+    CK(dalloc(&h->Xh, dense));
+    CK(dalloc(&h->Yh, dense));
+  }
+  CK(cudaMemsetAsync(h->d_err, 0x7f, sizeof(int32_t), st));
+  if (h->timing) CK(cudaEventRecord(h->ev[2], st));
+  h->launches += launch_ldl_y(h, y_E, st);
+  if (h->timing) CK(cudaEventRecord(h->ev[3], st));
+  int32_t v;
+  sdpc_status s = check_err(h, st, &v);
+  if (s != SDPC_OK) return s;
+  if (v != kNoError) {
+    h->last_info = v;
+    return SDPC_ERR_NOT_PD;
+  }
+  h->have_y = true;
+  h->launches += launch_inverse_panels(h, st);
+  if (h->timing) CK(cudaEventRecord(h->ev[4], st));
+  h->launches += launch_scm(h, B, ldb, st);
+  if (h->timing) CK(cudaEventRecord(h->ev[5], st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (h->timing) {
+    h->times[1] = elapsed(h->ev[2], h->ev[3]);
+    h->times[2] = elapsed(h->ev[3], h->ev[4]);
+    h->times[3] = elapsed(h->ev[4], h->ev[5]);
+  }
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t ncols, double* X_out, double* Y_out,
+                                     void* stream) {
+  if (!h || !cols || ncols < 1 || !X_out || !Y_out) return SDPC_ERR_INVALID_ARG;
+  if (!h->have_y || !h->Xh) return SDPC_ERR_STATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int32_t> cn(ncols);
+  for (int32_t c = 0; c < ncols; ++c) {
+    if (cols[c] < 0 || cols[c] >= h->S.n) return SDPC_ERR_INVALID_ARG;
+    cn[c] = h->S.iperm[cols[c]];
+  }
+  int32_t* dc = nullptr;
+  CK(upload(&dc, cn));
+  h->launches += launch_gather_columns(h, dc, ncols, X_out, Y_out, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(dc);
+  CK(e);
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream) {
+  if (!h || !B || !info || ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(h->d_err, 0x7f, sizeof(int32_t), st));
+  if (h->timing) CK(cudaEventRecord(h->ev[6], st));
+  double fl = 0;
+  int nu = 0;
+  h->launches += potrf_lower(h, B, h->S.m, ldb, h->d_err, st, &fl, &nu);
+  if (h->timing) CK(cudaEventRecord(h->ev[7], st));
+  int32_t v;
+  sdpc_status s = check_err(h, st, &v);
+  if (s != SDPC_OK) return s;
+  if (h->timing) {
+    h->times[4] = elapsed(h->ev[6], h->ev[7]);
+    double tu = 0;
+    for (int i = 0; i < nu; ++i) tu += elapsed(h->upd_ev[2 * i], h->upd_ev[2 * i + 1]);
+    h->times[5] = tu;
+    h->times[6] = nu;
+    h->times[7] = fl;
+  }
+  if (v != kNoError) {
+    *info = v;
+    h->last_info = v;
+    return SDPC_ERR_NOT_PD;
+  }
+  *info = 0;
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const double* y_E, double* rdiag,
+                                int32_t* info, void* stream) {
+  if (!h || !xbar_E || !y_E || !info) return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nnz = h->S.nnzE(), m = h->S.m;
+  const int64_t ldb = m + (m & 1);
+  if (!h->Bown) {
+    CK(dalloc(&h->Bown, (size_t)ldb * m));
+    CK(dalloc(&h->xin, (size_t)std::max(nnz, m)));
+    CK(dalloc(&h->yin, (size_t)nnz));
+    CK(cudaMallocHost(&h->pinned_in, sizeof(double) * 2 * nnz));
+    CK(cudaMallocHost(&h->pinned_out, sizeof(double) * m));
+  }
+  std::memcpy(h->pinned_in, xbar_E, sizeof(double) * nnz);
+  std::memcpy(h->pinned_in + nnz, y_E, sizeof(double) * nnz);
+  CK(cudaMemcpyAsync(h->xin, h->pinned_in, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(h->yin, h->pinned_in + nnz, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  sdpc_status s = sdpc_factor_xinv(h, h->xin, stream);
+  if (s != SDPC_OK) return s;
+  s = sdpc_scm_build(h, h->yin, h->Bown, ldb, stream);
+  if (s != SDPC_OK) return s;
+  s = sdpc_scm_cholesky(h, h->Bown, ldb, info, stream);
+  if (s != SDPC_OK && s != SDPC_ERR_NOT_PD) return s;
+  if (rdiag) {
+    h->launches += launch_diag_copy(h->Bown, m, ldb, h->xin, st);
+    CK(cudaMemcpyAsync(h->pinned_out, h->xin, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(rdiag, h->pinned_out, sizeof(double) * m);
+  }
+  return s;
+}
+
+sdpc_status sdpc_fp64_peak(int32_t device, double ms, double* dmma_tflops, double* dfma_tflops) {
+  if (!dmma_tflops || !dfma_tflops) return SDPC_ERR_INVALID_ARG;
+  cudaError_t e = fp64_peak(device, ms, dmma_tflops, dfma_tflops);
+  return e == cudaSuccess ? SDPC_OK : SDPC_ERR_CUDA;
+}
+
+}  // extern "C"

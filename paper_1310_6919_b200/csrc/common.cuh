@@ -1,0 +1,41 @@
+// Shared device/host helpers for libsdpc kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+namespace sdpc {
+
+constexpr int kWarp = 32;
+constexpr int kPanelW = 32;  // RHS panel width of the multi-RHS solves: lane <-> RHS column
+
+// Device error flag protocol: kernels atomicMin the failing index into *err
+// (initialised to kNoError by a byte memset).  Host reads it after the phase.
+constexpr int32_t kNoError = 0x7f7f7f7f;  // = cudaMemset(.., 0x7f, 4)
+
+__device__ __forceinline__ void report_error(int32_t* err, int32_t idx) { atomicMin(err, idx); }
+
+// FP64 tensor-core MMA: D(8x8) = A(8x4, row) * B(4x8, col) + C.  Lowers to DMMA.8x8x4 on sm_100a.
+// Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// c/d = C[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+}  // namespace sdpc

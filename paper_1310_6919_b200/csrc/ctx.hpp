@@ -1,0 +1,118 @@
+// Internal handle state of libsdpc and the kernel launchers' interfaces.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "symbolic.hpp"
+
+namespace sdpc {
+
+// Device mirror of the symbolic structure (all arrays owned by the handle).
+struct DevSym {
+  int32_t n = 0, m = 0, nsuper = 0;
+  int64_t nnzE = 0;
+  int64_t* colptr = nullptr;
+  int32_t* rowind = nullptr;
+  int32_t* super_ptr = nullptr;
+  int32_t* snc = nullptr;
+  int32_t* sns = nullptr;
+  int32_t* sparent = nullptr;
+  int64_t* panel_off = nullptr;
+  int32_t* e2p = nullptr;
+  int64_t* umap_off = nullptr;
+  int32_t* umap = nullptr;
+  int64_t* relind_off = nullptr;
+  int32_t* relind = nullptr;
+  int64_t* upd_off = nullptr;
+  int32_t* child_ptr = nullptr;
+  int32_t* child_list = nullptr;
+  int32_t* hlev_sn = nullptr;   // supernodes sorted by height
+  int32_t* dlev_ptr = nullptr;  // depth level pointers (device copy)
+  int32_t* dlev_sn = nullptr;
+  int32_t* perm = nullptr;
+  int32_t* iperm = nullptr;
+  int32_t* reach_ptr = nullptr;  // per RHS panel: supernodes on the union of etree paths
+  int32_t* reach_sn = nullptr;
+  int32_t npanels = 0;
+};
+
+// Size classes of the batched per-clique kernels ((a1) and (a2)).
+struct CliqueClass {
+  int threads = 64;
+  size_t smem = 0;          // dynamic shared memory bytes (0 => global workspace)
+  std::vector<int32_t> sn;  // supernodes in this class
+  int32_t* d_sn = nullptr;
+};
+
+// Constraint data in elimination ids, symmetric-expanded (for (c)).
+struct DevCons {
+  bool maxcut = false;
+  int32_t m = 0;
+  int64_t* ptr = nullptr;  // [m+1]
+  int32_t* ei = nullptr;   // entry row (new id)
+  int32_t* ej = nullptr;   // entry col (new id)
+  double* ev = nullptr;
+  int32_t* large = nullptr;     // list of constraint ids with many entries
+  int32_t nlarge = 0;
+  uint8_t* is_large = nullptr;  // [m]
+  // max-cut fast path
+  int32_t* vrow = nullptr;      // [m] elimination row of constraint k's vertex
+  double* aval = nullptr;       // [m] value a_k
+  int32_t* col_cons = nullptr;  // [n] constraint index whose vertex is elimination column j, or -1
+};
+
+}  // namespace sdpc
+
+struct sdpc_ctx {
+  int device = 0;
+  int nranks = 1, rank = 0;
+  sdpc::Symbolic S;
+  sdpc::DevSym d;
+  sdpc::DevCons cons;
+  std::vector<sdpc::CliqueClass> a1cls, a2cls;  // per-level classes for (a2) are rebuilt per level
+  std::vector<std::vector<sdpc::CliqueClass>> a2lev;
+  double* ws = nullptr;          // global workspace for large cliques ((a1) and (a2))
+  int64_t* d_ws_off = nullptr;   // per supernode offset into ws (doubles), -1 if smem class
+  double* Lx = nullptr;          // X factor panels
+  double* Dx = nullptr;
+  double* Ly = nullptr;          // Y factor panels
+  double* Dy = nullptr;
+  double* upd = nullptr;         // multifrontal update matrices
+  double* Xh = nullptr;          // dense X-hat, panel-major [npanels][n][32]
+  double* Yh = nullptr;          // dense Y^{-1}
+  int32_t* d_err = nullptr;
+  double* Bown = nullptr;        // handle-owned B for sdpc_iteration_host
+  double* xin = nullptr;         // device staging for sdpc_iteration_host
+  double* yin = nullptr;
+  double* pinned_in = nullptr;   // pinned host staging (2*nnzE)
+  double* pinned_out = nullptr;  // pinned host staging (m)
+  double* potrf_ws = nullptr;    // inverse of the diagonal block (nb x nb)
+  bool have_x = false, have_y = false;
+  int64_t last_info = 0;
+  bool timing = true;
+  double times[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t launches = 0;
+  cudaEvent_t ev[16];
+  std::vector<cudaEvent_t> upd_ev;  // per trailing-update launch (pairs)
+  std::string err;
+};
+
+namespace sdpc {
+// Launchers (each returns number of kernels launched; errors via cudaGetLastError).
+int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st);
+int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st);
+int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st);
+int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st);
+int launch_panels_to_E(sdpc_ctx* h, const double* panels, double* E, cudaStream_t st);
+int launch_gather_columns(sdpc_ctx* h, const int32_t* d_cols_new, int32_t ncols, double* Xo, double* Yo,
+                          cudaStream_t st);
+// Dense FP64 Cholesky of the lower triangle of B (m x m, ld).  Returns launches; info via d_err
+// (1-based failing column, kNoError if ok).  If upd_times, records an event pair per trailing update.
+int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st, double* flops_upd,
+                int* n_upd);
+int launch_diag_copy(double* B, int64_t m, int64_t ld, double* out, cudaStream_t st);
+cudaError_t fp64_peak(int device, double ms, double* dmma, double* dfma);
+}  // namespace sdpc

@@ -1,0 +1,147 @@
+// (b) Multi-RHS supernodal solves: dense X-hat = (L D L^T)^{-1} and Y^{-1} = (L_Y D_Y L_Y^T)^{-1},
+// one RHS panel of 32 identity columns per CTA (lane <-> RHS column).
+//
+// PAPER.md P:320-330 (forward/backward substitution instead of forming X-hat),
+// P:686-688 (Eq. newSCM2: x_p = L-hat^{-T} L-hat^{-1} e_p, v = N^{-T} N^{-1} [A_j]_{*k}),
+// P:859-869 (reuse of x_p across a column of B; on B200 the whole X-hat fits in HBM, so the
+// columns are materialised once and reused by every column of B, SURVEY §8(a) notes).
+//
+// Per panel P (columns p0 = 32P .. p0+31, elimination order):
+//   forward  L z = E_P  over the union of the etree paths of the panel's columns (ascending
+//            supernodes; rows outside the paths are exactly zero);  z <- D^{-1} z;
+//   backward L^T x = z  over all supernodes, level by level from the roots (no write conflicts:
+//            a supernode writes only its own rows S_r and reads ancestors U_r).
+// Output layout: panel-major, X[P][i][lane] (row i of the panel = 32 contiguous doubles).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "ctx.hpp"
+
+namespace sdpc {
+
+struct SolveArgs {
+  int32_t n, nsuper, ndlev;
+  const int32_t* super_ptr;
+  const int32_t* snc;
+  const int32_t* sns;
+  const int64_t* colptr;
+  const int32_t* rowind;
+  const int64_t* panel_off;
+  const int32_t* reach_ptr;
+  const int32_t* reach_sn;
+  const int32_t* dlev_ptr;
+  const int32_t* dlev_sn;
+  const double* Lp[2];
+  const double* D[2];
+  double* out[2];
+};
+
+constexpr int kSolveThreads = 256;
+
+__global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs a) {
+  extern __shared__ uint32_t inreach[];  // bitmap over supernodes
+  const int P = blockIdx.x, fac = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = kSolveThreads / 32;
+  const int n = a.n;
+  const double* __restrict__ Lp = a.Lp[fac];
+  const double* __restrict__ D = a.D[fac];
+  double* X = a.out[fac] + (size_t)P * n * kPanelW;
+  const int p0 = P * kPanelW;
+  const int32_t* __restrict__ rowind = a.rowind;
+
+  const int nwords = (a.nsuper + 31) / 32;
+  for (int i = tid; i < nwords; i += kSolveThreads) inreach[i] = 0;
+  __syncthreads();
+  const int rb = a.reach_ptr[P], re = a.reach_ptr[P + 1];
+  for (int q = rb + tid; q < re; q += kSolveThreads) {
+    const int r = a.reach_sn[q];
+    atomicOr(&inreach[r >> 5], 1u << (r & 31));
+  }
+  __syncthreads();
+  // initialise z rows on the paths: z[i][lane] = (i == p0 + lane)
+  for (int q = rb + wid; q < re; q += NW) {
+    const int r = a.reach_sn[q];
+    const int f = a.super_ptr[r], s = a.sns[r];
+    for (int t = 0; t < s; ++t) X[(size_t)(f + t) * kPanelW + lane] = (f + t == p0 + lane) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  // forward L z = E_P over the paths, ascending supernodes
+  for (int q = rb; q < re; ++q) {
+    const int r = a.reach_sn[q];
+    const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
+    const double* Lr = Lp + a.panel_off[r];
+    if (wid == 0) {  // unit lower diagonal block
+      for (int t = 1; t < s; ++t) {
+        double acc = X[(size_t)(f + t) * kPanelW + lane];
+        for (int tp = 0; tp < t; ++tp) acc -= Lr[t + (size_t)tp * c] * X[(size_t)(f + tp) * kPanelW + lane];
+        X[(size_t)(f + t) * kPanelW + lane] = acc;
+      }
+    }
+    __syncthreads();
+    const int32_t* U = rowind + a.colptr[f] + s;
+    for (int qq = wid; qq < u; qq += NW) {
+      const int row = U[qq];
+      double acc = X[(size_t)row * kPanelW + lane];
+      for (int t = 0; t < s; ++t) acc -= Lr[s + qq + (size_t)t * c] * X[(size_t)(f + t) * kPanelW + lane];
+      X[(size_t)row * kPanelW + lane] = acc;
+    }
+    __syncthreads();
+    for (int t = wid; t < s; t += NW) X[(size_t)(f + t) * kPanelW + lane] /= D[f + t];
+  }
+  __syncthreads();
+
+  // backward L^T x = z, depth levels from the roots; rows off the paths have z = 0
+  for (int lv = 0; lv < a.ndlev; ++lv) {
+    for (int q = a.dlev_ptr[lv] + wid; q < a.dlev_ptr[lv + 1]; q += NW) {
+      const int r = a.dlev_sn[q];
+      const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
+      const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
+      const double* Lr = Lp + a.panel_off[r];
+      const int32_t* U = rowind + a.colptr[f] + s;
+      for (int t = s - 1; t >= 0; --t) {
+        double acc = onpath ? X[(size_t)(f + t) * kPanelW + lane] : 0.0;
+        const double* Lc = Lr + (size_t)t * c;
+        for (int qq = 0; qq < u; ++qq) acc -= Lc[s + qq] * X[(size_t)U[qq] * kPanelW + lane];
+        for (int tp = t + 1; tp < s; ++tp) acc -= Lc[tp] * X[(size_t)(f + tp) * kPanelW + lane];
+        X[(size_t)(f + t) * kPanelW + lane] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
+  SolveArgs a{};
+  a.n = h->S.n;
+  a.nsuper = h->S.nsuper;
+  a.ndlev = (int32_t)h->S.dlev_ptr.size() - 1;
+  a.super_ptr = h->d.super_ptr;
+  a.snc = h->d.snc;
+  a.sns = h->d.sns;
+  a.colptr = h->d.colptr;
+  a.rowind = h->d.rowind;
+  a.panel_off = h->d.panel_off;
+  a.reach_ptr = h->d.reach_ptr;
+  a.reach_sn = h->d.reach_sn;
+  a.dlev_ptr = h->d.dlev_ptr;
+  a.dlev_sn = h->d.dlev_sn;
+  a.Lp[0] = h->Lx;
+  a.Lp[1] = h->Ly;
+  a.D[0] = h->Dx;
+  a.D[1] = h->Dy;
+  a.out[0] = h->Xh;
+  a.out[1] = h->Yh;
+  size_t smem = sizeof(uint32_t) * ((h->S.nsuper + 31) / 32);
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid(h->d.npanels, 2);
+  inverse_panel_kernel<<<grid, kSolveThreads, smem, st>>>(a);
+  return 1;
+}
+
+}  // namespace sdpc
