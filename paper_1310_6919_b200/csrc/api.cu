@@ -44,7 +44,8 @@ sdpc_status map_cuda(sdpc_ctx* h, cudaError_t e) {
     if (_e != cudaSuccess) return map_cuda(h, _e); \
   } while (0)
 
-constexpr size_t kSmemCap = 220 * 1024;
+constexpr size_t kSmemCap = 200 * 1024;   // dynamic smem per clique CTA (static ~8.5 KB on top)
+constexpr size_t kPanelCap = 200 * 1024;  // shared-memory panel of a global-workspace clique
 
 // size classes for the per-clique kernels
 int class_of(size_t bytes) {
@@ -53,16 +54,18 @@ int class_of(size_t bytes) {
   if (bytes <= kSmemCap) return 2;
   return 3;
 }
-const int kClassThreads[4] = {64, 128, 256, 512};
+const int kClassThreads[4] = {64, 128, 256, 256};
 
 cudaError_t build_classes(std::vector<CliqueClass>& cls, const std::vector<int32_t>& members,
-                          const std::vector<size_t>& bytes, const std::vector<int64_t>& ws_off) {
+                          const std::vector<size_t>& bytes, const std::vector<int64_t>& ws_off,
+                          const std::vector<size_t>& panel_bytes) {
   cls.assign(4, CliqueClass{});
   for (int q = 0; q < 4; ++q) cls[q].threads = kClassThreads[q];
   for (int32_t r : members) {
     int q = ws_off[r] >= 0 ? 3 : class_of(bytes[r]);
     cls[q].sn.push_back(r);
     if (q < 3) cls[q].smem = std::max(cls[q].smem, bytes[r]);
+    else cls[q].smem = std::max(cls[q].smem, std::min(kPanelCap, panel_bytes[r]));
   }
   // biggest cliques first so the long CTAs start early
   for (auto& k : cls) {
@@ -159,28 +162,29 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   };
 
   // ---- per-clique size classes and global workspace
-  std::vector<size_t> b1(ns), b2(ns);
+  std::vector<size_t> b1(ns), b2(ns), pb(ns);
   std::vector<int64_t> ws_off(ns, -1);
   int64_t ws_total = 0;
   for (int32_t r = 0; r < ns; ++r) {
     const size_t c = S.snc[r], s = S.sns[r];
     b1[r] = (c * c + c * s) * sizeof(double);
     b2[r] = c * c * sizeof(double);
+    pb[r] = c * 32 * sizeof(double);
     if (b1[r] > kSmemCap) {
       ws_off[r] = ws_total;
-      ws_total += (int64_t)(c * c + c * s);
+      ws_total += (int64_t)(c * c + c * s + c * 32);  // A, W, and a panel fallback if c*32 > kPanelCap
     }
   }
   std::vector<int32_t> all(ns);
   for (int32_t r = 0; r < ns; ++r) all[r] = r;
   std::stable_sort(all.begin(), all.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
-  if (build_classes(h->a1cls, all, b1, ws_off) != cudaSuccess) return fail(SDPC_ERR_OOM);
+  if (build_classes(h->a1cls, all, b1, ws_off, pb) != cudaSuccess) return fail(SDPC_ERR_OOM);
   const int nh = (int)S.hlev_ptr.size() - 1;
   h->a2lev.resize(nh);
   for (int lv = 0; lv < nh; ++lv) {
     std::vector<int32_t> mem(S.hlev_sn.begin() + S.hlev_ptr[lv], S.hlev_sn.begin() + S.hlev_ptr[lv + 1]);
     std::stable_sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
-    if (build_classes(h->a2lev[lv], mem, b2, ws_off) != cudaSuccess) return fail(SDPC_ERR_OOM);
+    if (build_classes(h->a2lev[lv], mem, b2, ws_off, pb) != cudaSuccess) return fail(SDPC_ERR_OOM);
   }
 
   // ---- RHS panels: union of the etree paths of each panel's columns (supernode granularity)
@@ -310,7 +314,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   AL(h->Dy, (size_t)n);
   AL(h->upd, (size_t)S.upd_total);
   AL(h->d_err, 1);
-  AL(h->potrf_ws, 128 * 128);
+  AL(h->potrf_ws, 2 * 128 * 128);
 #undef AL
   for (auto& ev : h->ev) cudaEventCreate(&ev);
   if (cudaGetLastError() != cudaSuccess) return fail(SDPC_ERR_CUDA);
@@ -337,6 +341,9 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   for (auto& ev : h->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : h->upd_ev) cudaEventDestroy(ev);
+  if (h->evA) cudaEventDestroy(h->evA);
+  if (h->evB) cudaEventDestroy(h->evB);
+  if (h->st2) cudaStreamDestroy(h->st2);
   delete h;
   return SDPC_OK;
 }

@@ -89,7 +89,9 @@ struct sdpc_ctx {
   double* yin = nullptr;
   double* pinned_in = nullptr;   // pinned host staging (2*nnzE)
   double* pinned_out = nullptr;  // pinned host staging (m)
-  double* potrf_ws = nullptr;    // inverse of the diagonal block (nb x nb)
+  double* potrf_ws = nullptr;    // inverses of the diagonal blocks (2 x nb x nb, double-buffered)
+  cudaStream_t st2 = nullptr;    // lookahead stream of the SCM Cholesky
+  cudaEvent_t evA = nullptr, evB = nullptr;
   bool have_x = false, have_y = false;
   int64_t last_info = 0;
   bool timing = true;

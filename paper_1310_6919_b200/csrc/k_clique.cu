@@ -2,13 +2,18 @@
 //
 // (a1) PAPER.md P:493-530, Algorithm 1.  One CTA per clique r (fundamental supernode):
 //      Step 2-1 gather P_r X-bar_{C_rC_r} P_r^T (reversal is index arithmetic),
-//      Step 2-2 Cholesky = M_r M_r^T in shared memory (global workspace for big cliques),
+//      Step 2-2 Cholesky = M_r M_r^T,
 //      Step 2-3 L_r = P_r M_r^{-T} P_r^T: only its first |S_r| columns are needed (Step 3),
 //      i.e. the last |S_r| rows of M_r^{-1}, obtained by back substitution M_r^T W = [0; I].
 //      Output in the north-star unit form L-hat = L D^{1/2}: D_j = L-hat_jj^2, L = L-hat / L-hat_jj.
 // (a2) PAPER.md P:221-225 / P:722-725 (type (v)): Y = L_Y D_Y L_Y^T on the same E, multifrontal:
-//      frontal = Y[C_r, S_r] + extend-add of the children's update matrices, partial LDL^T of
-//      the |S_r| pivot columns, Schur complement passed to the parent.  One launch per etree height.
+//      frontal = Y[C_r, S_r] + extend-add of the children's update matrices, Cholesky of the
+//      |S_r| pivot columns, Schur complement passed to the parent.  One launch per etree height.
+// Both use the same CTA-cooperative dense routines, blocked by 32 columns: the 32 x 32 diagonal
+// block is factored and inverted by one warp in registers (shuffles), the panel below is formed
+// with the inverse, and the trailing matrix is updated with 4 x 4 register tiles per thread.
+// Cliques whose working set exceeds shared memory live in an L2-resident global workspace; their
+// current 32-column panel is staged in shared memory.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -38,16 +43,216 @@ struct CliqueArgs {
   double* upd;
 };
 
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr int kLdInv = 33;
+
+// Shared-memory scratch layout for one CTA: inverse of the current 32 x 32 diagonal block, and
+// (global-workspace cliques) the current panel P (c x 32, ld c).
+struct Scratch {
+  double* inv;    // 32 x 33
+  double* l11;    // 32 x 33 staging of the factored diagonal block
+  double* panel;  // c x 32 (only used when the matrix lives in global memory)
+  int* flag;
+};
+
+// Warp 0: Cholesky of the jw x jw block at A[j0, j0] in registers (lane = row), write it back,
+// then invert it (lane = column) into s.inv (lower, zero-padded to 32 x 32).  Returns via *flag
+// the failing local column (>= 0) or -1.
+__device__ __forceinline__ void warp_chol_inv32(double* A, int ld, int j0, int jw, const Scratch& s) {
+  const int lane = threadIdx.x & 31;
+  double row[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    row[c] = (lane < jw && c < jw) ? A[(j0 + lane) + (size_t)(j0 + c) * ld] : (lane == c ? 1.0 : 0.0);
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(kFullMask, row[j], j);
+    if (fail < 0) {
+      if (!(d > 0.0)) {
+        fail = j;
+      } else {
+        const double l = sqrt(d);
+        if (lane == j) row[j] = l;
+        else if (lane > j) row[j] /= l;
+#pragma unroll
+        for (int k = j + 1; k < 32; ++k) {
+          const double akj = __shfl_sync(kFullMask, row[j], k);
+          if (lane >= k) row[k] -= row[j] * akj;
+        }
+      }
+    }
+  }
+  if (lane == 0) *s.flag = fail;
+  if (fail >= 0) return;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const double v = lane >= c ? row[c] : 0.0;
+    s.l11[lane + c * kLdInv] = v;
+    if (lane < jw && c < jw) A[(j0 + lane) + (size_t)(j0 + c) * ld] = v;
+  }
+  __syncwarp();
+  // inverse: x = column `lane` of L11^{-1} by forward substitution (L11 broadcast from smem)
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double sacc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) sacc -= s.l11[i + k * kLdInv] * x[k];
+    x[i] = sacc / s.l11[i + i * kLdInv];
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s.inv[i + lane * kLdInv] = i >= lane ? x[i] : 0.0;
+}
+
+// CTA-cooperative blocked Cholesky of the leading `ncols` columns of the symmetric c x c matrix A
+// (lower triangle, column-major, leading dimension ld = c), with the trailing block updated.
+// Returns the failing column index, or -1.
+template <int NT, bool GLOBAL>
+__device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
+  const int tid = threadIdx.x, wid = tid >> 5;
+  const int ld = c;
+  for (int j0 = 0; j0 < ncols; j0 += 32) {
+    const int jw = min(32, ncols - j0);
+    if (wid == 0) warp_chol_inv32(A, ld, j0, jw, s);
+    __syncthreads();
+    const int f = *s.flag;
+    if (f >= 0) return j0 + f;
+    // panel below the diagonal block: L[i, j0:j0+jw] = A[i, j0:j0+jw] L11^{-T}
+    const int r0 = j0 + jw, nr = c - r0;
+    double* P = GLOBAL ? s.panel : A + (size_t)j0 * ld;  // P[i + k*ld] = L[i, j0+k]
+    if (nr > 0) {
+      // rows in groups of 2 x (jw outputs) per thread would need registers; do row-per-thread-chunk:
+      for (int idx = tid; idx < nr; idx += NT) {
+        const int i = r0 + idx;
+        double a[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) a[k] = k < jw ? A[i + (size_t)(j0 + k) * ld] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if (q < jw) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k <= q; ++k) acc += a[k] * s.inv[q + k * kLdInv];
+            P[i + (size_t)q * ld] = acc;
+            if (GLOBAL) A[i + (size_t)(j0 + q) * ld] = acc;
+          }
+        }
+      }
+      __syncthreads();
+      // trailing update of rows/cols >= r0: A[i,j] -= sum_k P[i,k] P[j,k], 4 x 4 register tiles
+      const int nb4 = (nr + 3) >> 2;
+      const int ntile = nb4 * (nb4 + 1) / 2;
+      for (int t = tid; t < ntile; t += NT) {
+        int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while (bi * (bi + 1) / 2 > t) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+        const int bj = t - bi * (bi + 1) / 2;
+        const int i0 = r0 + bi * 4, jj0 = r0 + bj * 4;
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int k = 0; k < jw; ++k) {
+          double pi[4], pj[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) pi[a] = (i0 + a < c) ? P[i0 + a + (size_t)k * ld] : 0.0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) pj[b] = (jj0 + b < c) ? P[jj0 + b + (size_t)k * ld] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] += pi[a] * pj[b];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int i = i0 + a, j = jj0 + b;
+            if (i < c && j < c && i >= j) A[i + (size_t)j * ld] -= acc[a][b];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  return -1;
+}
+
+// W (c x s, ld c) = M^{-T} [0; I_s]: blocked back substitution from the last 32-row block up.
+// M lower (A, ld c).  Column t of W is nonzero only in rows <= u + t.
 template <int NT>
-__global__ void __launch_bounds__(NT) alg1_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
+__device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, const Scratch& sc) {
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int u = c - s;
+  for (int idx = tid; idx < c * s; idx += NT) {
+    const int i = idx % c, t = idx / c;
+    W[idx] = (i == u + t) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int nblk = (c + 31) / 32;
+  for (int bI = nblk - 1; bI >= 0; --bI) {
+    const int jb = bI * 32, jw = min(32, c - jb);
+    const int t0 = jb > u ? jb - u : 0;  // columns t < t0 are zero in rows >= jb
+    const int ns = s - t0;
+    // W[J, t] -= sum_{i >= jb+jw} M[i, jb+q] W[i, t]
+    const int lo = jb + jw;
+    if (lo < c && ns > 0) {
+      for (int idx = tid; idx < jw * ns; idx += NT) {
+        const int q = idx % jw, t = t0 + idx / jw;
+        const double* Mc = A + (size_t)(jb + q) * c;
+        const double* Wc = W + (size_t)t * c;
+        const int hi = min(c, u + t + 1);  // W[i, t] = 0 for i > u + t
+        double acc = 0.0;
+        for (int i = lo; i < hi; ++i) acc += Mc[i] * Wc[i];
+        W[jb + q + (size_t)t * c] -= acc;
+      }
+    }
+    // inverse of the diagonal block M[J,J] (lower): warp 0
+    if (wid == 0) {
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        double sacc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) sacc -= ((i < jw && k < jw) ? A[(jb + i) + (size_t)(jb + k) * c] : 0.0) * x[k];
+        const double dii = (i < jw) ? A[(jb + i) + (size_t)(jb + i) * c] : 1.0;
+        x[i] = sacc / dii;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) sc.inv[i + lane * kLdInv] = i >= lane ? x[i] : 0.0;
+    }
+    __syncthreads();
+    // W[J, t] = M[J,J]^{-T} W[J, t]:  W_new[q] = sum_{p >= q} inv[p][q] W_old[p], one thread per column t
+    for (int t = t0 + tid; t < s; t += NT) {
+      double w[32];
+#pragma unroll
+      for (int p = 0; p < 32; ++p) w[p] = p < jw ? W[jb + p + (size_t)t * c] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        if (q < jw) {
+          double acc = 0.0;
+#pragma unroll
+          for (int p = q; p < 32; ++p) acc += sc.inv[p + q * kLdInv] * w[p];
+          W[jb + q + (size_t)t * c] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) alg1_kernel(CliqueArgs a, const int32_t* __restrict__ list, int pbytes) {
   extern __shared__ double smem[];
-  __shared__ int bad;
+  __shared__ double inv[32 * kLdInv], l11[32 * kLdInv];
+  __shared__ int flag;
   const int r = list[blockIdx.x];
   const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
-  double* A = (a.ws_off[r] >= 0) ? a.ws + a.ws_off[r] : smem;
+  const bool glob = a.ws_off[r] >= 0;
+  double* A = glob ? a.ws + a.ws_off[r] : smem;
   double* W = A + (size_t)c * c;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x;
   const int64_t* __restrict__ colptr = a.colptr;
   const double* __restrict__ X = a.vals;
 
@@ -66,48 +271,18 @@ __global__ void __launch_bounds__(NT) alg1_kernel(CliqueArgs a, const int32_t* _
     }
     A[idx] = v;
   }
-  for (int idx = tid; idx < c * s; idx += NT) {
-    const int i = idx % c, t = idx / c;
-    W[idx] = (i == u + t) ? 1.0 : 0.0;
-  }
-  if (tid == 0) bad = 0;
   __syncthreads();
-
-  // Step 2-2: Cholesky A = M M^T (right-looking, lower).
-  for (int k = 0; k < c; ++k) {
-    if (tid == 0) {
-      const double d = A[k + (size_t)k * c];
-      if (!(d > 0.0)) bad = 1;
-      else A[k + (size_t)k * c] = sqrt(d);
-    }
-    __syncthreads();
-    if (bad) {
-      if (tid == 0) report_error(a.err, r);
-      return;
-    }
-    const double inv = 1.0 / A[k + (size_t)k * c];
-    for (int i = k + 1 + tid; i < c; i += NT) A[i + (size_t)k * c] *= inv;
-    __syncthreads();
-    for (int j = k + 1 + wid; j < c; j += NW) {
-      const double ajk = A[j + (size_t)k * c];
-      for (int i = j + lane; i < c; i += 32) A[i + (size_t)j * c] -= A[i + (size_t)k * c] * ajk;
-    }
-    __syncthreads();
+  // global cliques: the current 32-column panel goes to shared memory if it fits, else after W
+  double* panel = ((size_t)c * 32 * sizeof(double) <= (size_t)pbytes) ? smem : W + (size_t)c * s;
+  Scratch sc{inv, l11, panel, &flag};
+  // Step 2-2: Cholesky A = M M^T
+  int fail = glob ? cta_chol_partial<NT, true>(A, c, c, sc) : cta_chol_partial<NT, false>(A, c, c, sc);
+  if (fail >= 0) {
+    if (tid == 0) report_error(a.err, r);
+    return;
   }
-
-  // Step 2-3 (first |S_r| columns only): M^T W = [0; I_s], back substitution.
-  for (int jp = c - 1; jp >= 0; --jp) {
-    const int t0 = jp > u ? jp - u : 0;  // W[jp, t] = 0 for u + t < jp
-    const double inv = 1.0 / A[jp + (size_t)jp * c];
-    for (int t = t0 + tid; t < s; t += NT) W[jp + (size_t)t * c] *= inv;
-    __syncthreads();
-    const int ns = s - t0;
-    for (int idx = tid; idx < jp * ns; idx += NT) {
-      const int i = idx % jp, t = t0 + idx / jp;
-      W[i + (size_t)t * c] -= A[jp + (size_t)i * c] * W[jp + (size_t)t * c];
-    }
-    __syncthreads();
-  }
+  // Step 2-3 (first |S_r| columns only): M^T W = [0; I_s]
+  cta_backsub_last_rows<NT>(A, W, c, s, sc);
 
   // Step 3: L-hat[a, t] = W[c-1-a, s-1-t]; unit form L = L-hat / L-hat_tt, D = L-hat_tt^2.
   double* Lp = a.Lp + a.panel_off[r];
@@ -126,14 +301,15 @@ __global__ void __launch_bounds__(NT) alg1_kernel(CliqueArgs a, const int32_t* _
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
+__global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __restrict__ list, int pbytes) {
   extern __shared__ double smem[];
-  __shared__ int bad;
+  __shared__ double inv[32 * kLdInv], l11[32 * kLdInv];
+  __shared__ int flag;
   const int r = list[blockIdx.x];
   const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
-  double* F = (a.ws_off[r] >= 0) ? a.ws + a.ws_off[r] : smem;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  constexpr int NW = NT / 32;
+  const bool glob = a.ws_off[r] >= 0;
+  double* F = glob ? a.ws + a.ws_off[r] : smem;
+  const int tid = threadIdx.x;
   const int64_t* __restrict__ colptr = a.colptr;
 
   // frontal matrix: pivot columns from Y on E, the U x U block starts at zero
@@ -141,7 +317,6 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
     const int i = idx % c, j = idx / c;
     F[idx] = (j < s && i >= j) ? a.vals[colptr[f + j] + (i - j)] : 0.0;
   }
-  if (tid == 0) bad = 0;
   __syncthreads();
   // extend-add of the children's update matrices (sequential over children: deterministic)
   for (int q = a.child_ptr[r]; q < a.child_ptr[r + 1]; ++q) {
@@ -155,29 +330,24 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
     }
     __syncthreads();
   }
-  // partial LDL^T of the |S_r| pivot columns
-  for (int k = 0; k < s; ++k) {
-    const double d = F[k + (size_t)k * c];
-    if (!(d > 0.0)) {
-      if (tid == 0) report_error(a.err, f + k);
-      return;
-    }
-    const double inv = 1.0 / d;
-    __syncthreads();
-    for (int i = k + 1 + tid; i < c; i += NT) F[i + (size_t)k * c] *= inv;
-    __syncthreads();
-    for (int j = k + 1 + wid; j < c; j += NW) {
-      const double ljd = F[j + (size_t)k * c] * d;
-      for (int i = j + lane; i < c; i += 32) F[i + (size_t)j * c] -= F[i + (size_t)k * c] * ljd;
-    }
-    __syncthreads();
+  // Cholesky of the |S_r| pivot columns (L~ = L D^{1/2}) with the Schur complement in F_UU
+  double* panel = ((size_t)c * 32 * sizeof(double) <= (size_t)pbytes) ? smem : F + (size_t)c * c + (size_t)c * s;
+  Scratch sc{inv, l11, panel, &flag};
+  const int fail = glob ? cta_chol_partial<NT, true>(F, c, s, sc) : cta_chol_partial<NT, false>(F, c, s, sc);
+  if (fail >= 0) {
+    if (tid == 0) report_error(a.err, f + fail);
+    return;
   }
   double* Lp = a.Lp + a.panel_off[r];
   for (int idx = tid; idx < c * s; idx += NT) {
     const int ar = idx % c, t = idx / c;
-    Lp[idx] = ar > t ? F[idx] : (ar == t ? 1.0 : 0.0);
+    const double dg = F[t + (size_t)t * c];
+    Lp[idx] = ar > t ? F[idx] / dg : (ar == t ? 1.0 : 0.0);
   }
-  for (int t = tid; t < s; t += NT) a.D[f + t] = F[t + (size_t)t * c];
+  for (int t = tid; t < s; t += NT) {
+    const double dg = F[t + (size_t)t * c];
+    a.D[f + t] = dg * dg;
+  }
   if (u > 0) {
     double* Ur = a.upd + a.upd_off[r];
     for (int idx = tid; idx < u * u; idx += NT) {
@@ -185,7 +355,6 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
       Ur[idx] = ia >= ib ? F[(s + ia) + (size_t)(s + ib) * c] : 0.0;
     }
   }
-  (void)bad;
 }
 
 static CliqueArgs base_args(sdpc_ctx* h) {
@@ -214,10 +383,10 @@ static void launch_one(const CliqueArgs& a, const CliqueClass& k, cudaStream_t s
   static bool attr_done = false;
   auto fn = ALG1 ? alg1_kernel<NT> : mf_kernel<NT>;
   if (!attr_done) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
-  fn<<<(unsigned)k.sn.size(), NT, k.smem, st>>>(a, k.d_sn);
+  fn<<<(unsigned)k.sn.size(), NT, k.smem, st>>>(a, k.d_sn, (int)k.smem);
 }
 
 template <bool ALG1>

@@ -1,15 +1,18 @@
 // (d) Dense FP64 Cholesky of the SCM, B = R R^T (lower, in place).
 // PAPER.md P:711-713 / P:735-736 / P:978-979 (type (i): LAPACK dense Cholesky with multithreaded BLAS).
 //
-// Blocked right-looking, nb = 128.  Per panel step k0:
-//   diag  : one CTA factors the kb x kb diagonal block in shared memory (32-wide sub-panels,
-//           warp-level unblocked kernel) and forms its triangular inverse (for the TRSM);
-//   trsm  : L21 = A21 L11^{-T} as an FP64 tensor-core GEMM with the explicit inverse;
-//   update: A22 -= L21 L21^T over the lower 128 x 128 tiles, FP64 tensor-core GEMM
-//           (mma.sync m8n8k4 f64 -> DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind),
-//           operands staged in shared memory by a 3-stage cp.async pipeline.
-// Non-PD: the first failing column (1-based, LAPACK potrf rule) is atomicMin'ed into *err and
-// every later kernel exits at entry.
+// Blocked right-looking, nb = 128, with depth-1 lookahead on a second stream.  Per panel step k:
+//   diag(k)   : one CTA factors the 128 x 128 diagonal block in shared memory (32 x 32 diagonal
+//               sub-blocks in registers with warp shuffles, the rest as small in-CTA products)
+//               and forms L11^{-1} for the TRSM;
+//   trsm(k)   : L21 = A21 L11^{-T} as an FP64 tensor-core GEMM with the explicit inverse;
+//   ucol(k)   : trailing update of block column k+1 only (one column of 128 x 128 tiles);
+//   diag(k+1), trsm(k+1) run on the side stream while
+//   urest(k)  : the rest of the trailing update A22 -= L21 L21^T runs on the main stream.
+// GEMMs: mma.sync m8n8k4 f64 (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind), 128 x 128 CTA tiles,
+// 8 warps x (64 x 32), operands staged in shared memory by a 3-stage cp.async pipeline.
+// Non-PD: the first failing column (1-based, LAPACK potrf rule) is atomicMin'ed into *err and every
+// later kernel exits at entry.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -20,98 +23,159 @@
 
 namespace sdpc {
 
-constexpr int kNB = 128;       // panel width
-constexpr int kTile = 128;     // GEMM tile (BM = BN)
-constexpr int kBK = 16;        // k-chunk per pipeline stage
+constexpr int kNB = 128;         // panel width
+constexpr int kTile = 128;       // GEMM tile (BM = BN)
+constexpr int kBK = 16;          // k-chunk per pipeline stage
 constexpr int kStages = 3;
 constexpr int kLdS = kTile + 4;  // smem row stride (doubles): conflict-free fragment loads
 constexpr int kGemmThreads = 256;
 
 // ------------------------------------------------------------------ diagonal block
 constexpr int kDiagThreads = 256;
-constexpr int kLdD = kNB + 1;
+constexpr int kLdD = kNB + 1;  // A[i + j*kLdD]
+constexpr int kLdI = 33;       // 32 x 32 inverse blocks, Di[I][a + b*kLdI]
+constexpr unsigned kFull = 0xffffffffu;
 
 __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
-  extern __shared__ double A[];  // kb x kb, column-major, ld kLdD
+  extern __shared__ double sm[];
+  double* A = sm;                   // 128 x 128 (ld 129), lower = L; strict upper holds Linv^T blocks
+  double* Di = A + kNB * kLdD;      // inverses of the four 32 x 32 diagonal blocks
+  double* Tm = Di + 4 * 32 * kLdI;  // scratch for the off-diagonal inverse blocks
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double* Bd = B + k0 + (size_t)k0 * ld;
-  for (int idx = tid; idx < kb * kb; idx += kDiagThreads) {
-    const int i = idx % kb, j = idx / kb;
-    A[i + j * kLdD] = i >= j ? Bd[i + (size_t)j * ld] : 0.0;
+  for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
+    const int i = idx % kNB, j = idx / kNB;
+    double v = 0.0;
+    if (i < kb && j < kb) v = i >= j ? Bd[i + (size_t)j * ld] : 0.0;
+    else if (i == j) v = 1.0;  // identity padding beyond kb
+    A[i + j * kLdD] = v;
   }
   if (tid == 0) bad = 0;
   __syncthreads();
-  for (int jb = 0; jb < kb; jb += 32) {
-    const int jw = min(32, kb - jb);
-    if (wid == 0) {  // unblocked Cholesky of the jw x jw sub-block, one warp
-      for (int j = jb; j < jb + jw; ++j) {
-        const double d = A[j + j * kLdD];
-        if (!(d > 0.0)) {
-          if (lane == 0) {
-            bad = 1;
-            report_error(err, k0 + j + 1);
+
+  for (int I = 0; I < 4; ++I) {
+    const int o = I * 32;
+    if (wid == 0) {
+      // Cholesky of the 32 x 32 diagonal block in registers: lane = row o+lane
+      double row[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) row[c] = A[(o + lane) + (o + c) * kLdD];
+      int fail = -1;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double d = __shfl_sync(kFull, row[j], j);
+        if (fail < 0) {
+          if (!(d > 0.0)) {
+            fail = j;
+          } else {
+            const double l = sqrt(d);
+            if (lane == j) row[j] = l;
+            else if (lane > j) row[j] /= l;
+#pragma unroll
+            for (int k = j + 1; k < 32; ++k) {
+              const double akj = __shfl_sync(kFull, row[j], k);
+              if (lane >= k) row[k] -= row[j] * akj;
+            }
           }
-          break;
         }
-        const double sq = sqrt(d);
-        const int i = jb + lane;
-        __syncwarp();
-        if (i == j) A[j + j * kLdD] = sq;
-        if (i > j && i < jb + jw) A[i + j * kLdD] /= sq;
-        __syncwarp();
-        for (int jj = j + 1; jj < jb + jw; ++jj)
-          if (i >= jj && i < jb + jw) A[i + jj * kLdD] -= A[i + j * kLdD] * A[jj + j * kLdD];
-        __syncwarp();
+      }
+      if (fail >= 0) {
+        if (lane == 0) {
+          bad = 1;
+          report_error(err, k0 + o + fail + 1);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) A[(o + lane) + (o + c) * kLdD] = lane >= c ? row[c] : 0.0;
       }
     }
     __syncthreads();
     if (bad) return;
-    // rows below the sub-block: forward substitution against the sub-block (row-parallel)
-    for (int i = jb + jw + tid; i < kb; i += kDiagThreads) {
-      for (int j = jb; j < jb + jw; ++j) {
-        double a = A[i + j * kLdD];
-        for (int t = jb; t < j; ++t) a -= A[i + t * kLdD] * A[j + t * kLdD];
-        A[i + j * kLdD] = a / A[j + j * kLdD];
+    if (wid == 1) {
+      // inverse of the 32 x 32 lower block: lane = column j, forward substitution
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) s -= A[(o + i) + (o + k) * kLdD] * x[k];
+        x[i] = s / A[(o + i) + (o + i) * kLdD];
       }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) Di[I * 32 * kLdI + i + lane * kLdI] = i >= lane ? x[i] : 0.0;
+    }
+    __syncthreads();
+    if (I == 3) break;
+    // panel below: L[r, o:o+32] = A[r, o:o+32] * Linv_II^T   (rows r >= o+32)
+    const int r0 = o + 32, nr = kNB - r0;
+    const double* DI = Di + I * 32 * kLdI;
+    double vals[12];
+    int cnt = 0;
+    for (int idx = tid; idx < nr * 32; idx += kDiagThreads, ++cnt) {
+      const int r = r0 + idx % nr, c = idx / nr;
+      double s = 0.0;
+      for (int k = 0; k <= c; ++k) s += A[r + (o + k) * kLdD] * DI[c + k * kLdI];
+      vals[cnt] = s;
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int idx = tid; idx < nr * 32; idx += kDiagThreads, ++cnt) {
+      const int r = r0 + idx % nr, c = idx / nr;
+      A[r + (o + c) * kLdD] = vals[cnt];
     }
     __syncthreads();
     // trailing update of the diagonal block
-    const int r0 = jb + jw, nr = kb - r0;
     for (int idx = tid; idx < nr * nr; idx += kDiagThreads) {
       const int i = r0 + idx % nr, j = r0 + idx / nr;
       if (i < j) continue;
       double a = A[i + j * kLdD];
-      for (int t = jb; t < jb + jw; ++t) a -= A[i + t * kLdD] * A[j + t * kLdD];
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) a -= A[i + (o + t) * kLdD] * A[j + (o + t) * kLdD];
       A[i + j * kLdD] = a;
     }
     __syncthreads();
   }
+  // write L back to B (lower part of the kb x kb block)
   for (int idx = tid; idx < kb * kb; idx += kDiagThreads) {
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
-  __syncthreads();
-  // triangular inverse in place (LAPACK dtrti2 'L' order: columns from the last one)
-  __shared__ double tmp[kNB];
-  for (int j = kb - 1; j >= 0; --j) {
-    const double ajj = 1.0 / A[j + j * kLdD];
-    // x = T * A[j+1:, j] with T = already inverted trailing block, then scale by -ajj
-    for (int i = j + 1 + tid; i < kb; i += kDiagThreads) {
+  // off-diagonal blocks of L^{-1}: Linv[I,J] = -Di[I] * sum_{K=J}^{I-1} L[I,K] Linv[K,J], by distance d = I-J.
+  // Linv[K,J] for K > J is kept transposed in A's strict upper triangle: A[(J*32+b) + (K*32+a)*kLdD].
+  for (int d = 1; d < 4; ++d) {
+    const int npair = 4 - d;
+    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
+      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
+      const int J = p, I = p + d;
       double s = 0.0;
-      for (int t = j + 1; t <= i; ++t) s += A[i + t * kLdD] * A[t + j * kLdD];
-      tmp[i] = -ajj * s;
+      for (int K = J; K < I; ++K) {
+        for (int k = 0; k < 32; ++k) {
+          const double lik = A[(I * 32 + a) + (K * 32 + k) * kLdD];
+          const double xkj = (K == J) ? Di[J * 32 * kLdI + k + b * kLdI] : A[(J * 32 + b) + (K * 32 + k) * kLdD];
+          s += lik * xkj;
+        }
+      }
+      Tm[p * 32 * kLdI + a + b * kLdI] = s;
     }
     __syncthreads();
-    for (int i = j + 1 + tid; i < kb; i += kDiagThreads) A[i + j * kLdD] = tmp[i];
-    if (tid == 0) A[j + j * kLdD] = ajj;
+    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
+      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
+      const int J = p, I = p + d;
+      double s = 0.0;
+      for (int k = 0; k <= a; ++k) s -= Di[I * 32 * kLdI + a + k * kLdI] * Tm[p * 32 * kLdI + k + b * kLdI];
+      A[(J * 32 + b) + (I * 32 + a) * kLdD] = s;
+    }
     __syncthreads();
   }
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
     const int i = idx % kNB, j = idx / kNB;
-    Linv[idx] = (i < kb && j < kb && i >= j) ? A[i + j * kLdD] : 0.0;
+    const int I = i >> 5, J = j >> 5;
+    double v = 0.0;
+    if (i < kb && j < kb && i >= j) v = (I == J) ? Di[I * 32 * kLdI + (i & 31) + (j & 31) * kLdI] : A[j + i * kLdD];
+    Linv[idx] = v;
   }
 }
 
@@ -129,23 +193,30 @@ struct GemmArgs {
   const int32_t* err;
 };
 
-template <bool SYRK, bool AL16>
+enum { kModeTrsm = 0, kModeSyrkAll = 1, kModeSyrkCol = 2, kModeSyrkRest = 3 };
+
+template <int MODE, bool AL16>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
   if (*g.err != kNoError) return;
   extern __shared__ double sm[];
-  double* As = sm;                                  // [kStages][kBK][kLdS]
-  double* Bs = sm + kStages * kBK * kLdS;           // [kStages][kBK][kLdS]
+  double* As = sm;                         // [kStages][kBK][kLdS]
+  double* Bs = sm + kStages * kBK * kLdS;  // [kStages][kBK][kLdS]
   int bi, bj;
-  if (SYRK) {
+  if (MODE == kModeSyrkAll || MODE == kModeSyrkRest) {
     const int t = blockIdx.x;
     bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
     while (bi * (bi + 1) / 2 > t) --bi;
     while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
     bj = t - bi * (bi + 1) / 2;
+    if (MODE == kModeSyrkRest) {
+      ++bi;
+      ++bj;
+    }
   } else {
     bi = blockIdx.x;
     bj = 0;
   }
+  constexpr bool SYRK = MODE != kModeTrsm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int wm = wid >> 2, wn = wid & 3;  // 2 x 4 warps, warp tile 64 x 32
   const int g8 = lane >> 2, t4 = lane & 3;
@@ -238,35 +309,57 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
 }
 
 static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(double); }
+static size_t diag_smem() { return ((size_t)kNB * kLdD + 7 * 32 * kLdI) * sizeof(double); }
+
+template <int MODE>
+static void launch_gemm(bool al16, int grid, const GemmArgs& g, cudaStream_t st) {
+  if (grid <= 0) return;
+  if (al16) gemm_nt_kernel<MODE, true><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
+  else gemm_nt_kernel<MODE, false><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
+}
+
+template <int MODE>
+static void set_gemm_attr() {
+  cudaFuncSetAttribute(gemm_nt_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
+  cudaFuncSetAttribute(gemm_nt_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
+}
 
 int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st, double* flops_upd,
                 int* n_upd) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(gemm_nt_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
-    cudaFuncSetAttribute(gemm_nt_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
-    cudaFuncSetAttribute(gemm_nt_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
-    cudaFuncSetAttribute(gemm_nt_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
+    cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem());
+    set_gemm_attr<kModeTrsm>();
+    set_gemm_attr<kModeSyrkAll>();
+    set_gemm_attr<kModeSyrkCol>();
+    set_gemm_attr<kModeSyrkRest>();
     attr = true;
   }
+  if (!h->st2) {
+    cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->evA, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->evB, cudaEventDisableTiming);
+  }
+  cudaStream_t s2 = h->st2;
   const bool al16 = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+  const bool tim = h->timing;
   int launches = 0;
   double fl = 0.0;
   int nu = 0;
-  const bool tim = h && h->timing;
-  for (int64_t k0 = 0; k0 < m; k0 += kNB) {
+  const int64_t nsteps = (m + kNB - 1) / kNB;
+  auto panel = [&](int64_t k, cudaStream_t s) {  // diag(k) + trsm(k)
+    const int64_t k0 = k * kNB;
     const int kb = (int)std::min<int64_t>(kNB, m - k0);
-    potrf_diag_kernel<<<1, kDiagThreads, (size_t)kb * kLdD * sizeof(double), st>>>(B, ld, (int)k0, kb,
-                                                                                 h->potrf_ws, d_err);
+    double* Lw = h->potrf_ws + (k & 1) * kNB * kNB;
+    potrf_diag_kernel<<<1, kDiagThreads, diag_smem(), s>>>(B, ld, (int)k0, kb, Lw, d_err);
     ++launches;
     const int64_t base = k0 + kb;
     const int rows = (int)(m - base);
-    if (rows <= 0) break;
+    if (rows <= 0) return;
     GemmArgs g{};
     g.A = B + base + (size_t)k0 * ld;
     g.lda = ld;
-    g.Bm = h->potrf_ws;
+    g.Bm = Lw;
     g.ldbm = kNB;
     g.C = B + base + (size_t)k0 * ld;
     g.ldc = ld;
@@ -274,30 +367,54 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     g.cols = kb;
     g.K = kb;
     g.err = d_err;
-    const int T = (rows + kTile - 1) / kTile;
-    if (al16) gemm_nt_kernel<false, true><<<T, kGemmThreads, gemm_smem(), st>>>(g);
-    else gemm_nt_kernel<false, false><<<T, kGemmThreads, gemm_smem(), st>>>(g);
+    launch_gemm<kModeTrsm>(al16, (rows + kTile - 1) / kTile, g, s);
     ++launches;
-    GemmArgs u = g;
-    u.Bm = B + base + (size_t)k0 * ld;
+  };
+  panel(0, st);
+  for (int64_t k = 0; k < nsteps; ++k) {
+    const int64_t k0 = k * kNB;
+    const int kb = (int)std::min<int64_t>(kNB, m - k0);
+    const int64_t base = k0 + kb;
+    const int rows = (int)(m - base);
+    if (rows <= 0) break;
+    GemmArgs u{};
+    u.A = B + base + (size_t)k0 * ld;
+    u.lda = ld;
+    u.Bm = u.A;
     u.ldbm = ld;
     u.C = B + base + (size_t)base * ld;
-    if (tim) {
-      if ((int)h->upd_ev.size() < 2 * (nu + 1)) {
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        h->upd_ev.push_back(e0);
-        h->upd_ev.push_back(e1);
-      }
-      cudaEventRecord(h->upd_ev[2 * nu], st);
-    }
-    if (al16) gemm_nt_kernel<true, true><<<T * (T + 1) / 2, kGemmThreads, gemm_smem(), st>>>(u);
-    else gemm_nt_kernel<true, false><<<T * (T + 1) / 2, kGemmThreads, gemm_smem(), st>>>(u);
-    if (tim) cudaEventRecord(h->upd_ev[2 * nu + 1], st);
+    u.ldc = ld;
+    u.rows = rows;
+    u.cols = kb;
+    u.K = kb;
+    u.err = d_err;
+    const int T = (rows + kTile - 1) / kTile;
+    // block column k+1 first, then hand the next panel to the side stream
+    launch_gemm<kModeSyrkCol>(al16, T, u, st);
     ++launches;
-    ++nu;
-    fl += (double)rows * (double)(rows + 1) * (double)kb;
+    cudaEventRecord(h->evA, st);
+    cudaStreamWaitEvent(s2, h->evA, 0);
+    panel(k + 1, s2);
+    cudaEventRecord(h->evB, s2);
+    if (T > 1) {
+      if (tim) {
+        if ((int)h->upd_ev.size() < 2 * (nu + 1)) {
+          cudaEvent_t e0, e1;
+          cudaEventCreate(&e0);
+          cudaEventCreate(&e1);
+          h->upd_ev.push_back(e0);
+          h->upd_ev.push_back(e1);
+        }
+        cudaEventRecord(h->upd_ev[2 * nu], st);
+      }
+      launch_gemm<kModeSyrkRest>(al16, (T - 1) * T / 2, u, st);
+      if (tim) cudaEventRecord(h->upd_ev[2 * nu + 1], st);
+      ++launches;
+      ++nu;
+      const double r2 = (double)(rows - kTile);
+      fl += r2 * (r2 + 1.0) * (double)kb;
+    }
+    cudaStreamWaitEvent(st, h->evB, 0);
   }
   if (flops_upd) *flops_upd = fl;
   if (n_upd) *n_upd = nu;
