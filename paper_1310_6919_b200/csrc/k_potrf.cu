@@ -2,9 +2,8 @@
 // PAPER.md P:711-713 / P:735-736 / P:978-979 (type (i): LAPACK dense Cholesky with multithreaded BLAS).
 //
 // Blocked right-looking, nb = 128, with depth-1 lookahead on a second stream.  Per panel step k:
-//   diag(k)   : one CTA factors the 128 x 128 diagonal block in shared memory (32 x 32 diagonal
-//               sub-blocks in registers with warp shuffles, the rest as small in-CTA products)
-//               and forms L11^{-1} for the TRSM;
+//   diag(k)   : one CTA factors the 128 x 128 diagonal block in shared memory (whole CTA per
+//               column, two barriers per column) and forms L11^{-1} (thread per column) for the TRSM;
 //   trsm(k)   : L21 = A21 L11^{-T} as an FP64 tensor-core GEMM with the explicit inverse;
 //   ucol(k)   : trailing update of block column k+1 only (one column of 128 x 128 tiles);
 //   diag(k+1), trsm(k+1) run on the side stream while
@@ -33,18 +32,16 @@ constexpr int kGemmThreads = 256;
 // ------------------------------------------------------------------ diagonal block
 constexpr int kDiagThreads = 256;
 constexpr int kLdD = kNB + 1;  // A[i + j*kLdD]
-constexpr int kLdI = 33;       // 32 x 32 inverse blocks, Di[I][a + b*kLdI]
-constexpr unsigned kFull = 0xffffffffu;
 
 __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
   extern __shared__ double sm[];
-  double* A = sm;                   // 128 x 128 (ld 129), lower = L; strict upper holds Linv^T blocks
-  double* Di = A + kNB * kLdD;      // inverses of the four 32 x 32 diagonal blocks
-  double* Tm = Di + 4 * 32 * kLdI;  // scratch for the off-diagonal inverse blocks
+  double* A = sm;                 // 128 x 128 (ld 129): lower = L
+  double* X = A + kNB * kLdD;     // 128 x 128 (ld 129): L^{-1}, column c owned by thread c
+  __shared__ double col[2][kNB];  // scaled pivot column, double-buffered
   __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tid = threadIdx.x;
   double* Bd = B + k0 + (size_t)k0 * ld;
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
     const int i = idx % kNB, j = idx / kNB;
@@ -55,128 +52,59 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
   }
   if (tid == 0) bad = 0;
   __syncthreads();
-
-  for (int I = 0; I < 4; ++I) {
-    const int o = I * 32;
-    if (wid == 0) {
-      // Cholesky of the 32 x 32 diagonal block in registers: lane = row o+lane
-      double row[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) row[c] = A[(o + lane) + (o + c) * kLdD];
-      int fail = -1;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const double d = __shfl_sync(kFull, row[j], j);
-        if (fail < 0) {
-          if (!(d > 0.0)) {
-            fail = j;
-          } else {
-            const double l = sqrt(d);
-            if (lane == j) row[j] = l;
-            else if (lane > j) row[j] /= l;
-#pragma unroll
-            for (int k = j + 1; k < 32; ++k) {
-              const double akj = __shfl_sync(kFull, row[j], k);
-              if (lane >= k) row[k] -= row[j] * akj;
-            }
-          }
-        }
-      }
-      if (fail >= 0) {
-        if (lane == 0) {
-          bad = 1;
-          report_error(err, k0 + o + fail + 1);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) A[(o + lane) + (o + c) * kLdD] = lane >= c ? row[c] : 0.0;
-      }
+  // right-looking unblocked Cholesky, the whole CTA per column (2 barriers per column)
+  for (int j = 0; j < kNB; ++j) {
+    const double d = A[j + j * kLdD];
+    if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
+      if (tid == 0) report_error(err, k0 + j + 1);
+      return;
+    }
+    const double r = rsqrt(d);
+    double* cj = col[j & 1];
+    for (int i = j + tid; i < kNB; i += kDiagThreads) {
+      const double v = (i == j) ? d * r : A[i + j * kLdD] * r;
+      cj[i] = v;
+      A[i + j * kLdD] = v;
     }
     __syncthreads();
-    if (bad) return;
-    if (wid == 1) {
-      // inverse of the 32 x 32 lower block: lane = column j, forward substitution
-      double x[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; ++k) s -= A[(o + i) + (o + k) * kLdD] * x[k];
-        x[i] = s / A[(o + i) + (o + i) * kLdD];
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) Di[I * 32 * kLdI + i + lane * kLdI] = i >= lane ? x[i] : 0.0;
-    }
-    __syncthreads();
-    if (I == 3) break;
-    // panel below: L[r, o:o+32] = A[r, o:o+32] * Linv_II^T   (rows r >= o+32)
-    const int r0 = o + 32, nr = kNB - r0;
-    const double* DI = Di + I * 32 * kLdI;
-    double vals[12];
-    int cnt = 0;
-    for (int idx = tid; idx < nr * 32; idx += kDiagThreads, ++cnt) {
-      const int r = r0 + idx % nr, c = idx / nr;
-      double s = 0.0;
-      for (int k = 0; k <= c; ++k) s += A[r + (o + k) * kLdD] * DI[c + k * kLdI];
-      vals[cnt] = s;
-    }
-    __syncthreads();
-    cnt = 0;
-    for (int idx = tid; idx < nr * 32; idx += kDiagThreads, ++cnt) {
-      const int r = r0 + idx % nr, c = idx / nr;
-      A[r + (o + c) * kLdD] = vals[cnt];
-    }
-    __syncthreads();
-    // trailing update of the diagonal block
+    const int nr = kNB - j - 1;
     for (int idx = tid; idx < nr * nr; idx += kDiagThreads) {
-      const int i = r0 + idx % nr, j = r0 + idx / nr;
-      if (i < j) continue;
-      double a = A[i + j * kLdD];
-#pragma unroll 8
-      for (int t = 0; t < 32; ++t) a -= A[i + (o + t) * kLdD] * A[j + (o + t) * kLdD];
-      A[i + j * kLdD] = a;
+      const int ii = idx % nr, kk = idx / nr;
+      if (ii < kk) continue;
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      A[i + k * kLdD] -= cj[i] * cj[k];
     }
     __syncthreads();
   }
-  // write L back to B (lower part of the kb x kb block)
   for (int idx = tid; idx < kb * kb; idx += kDiagThreads) {
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
-  // off-diagonal blocks of L^{-1}: Linv[I,J] = -Di[I] * sum_{K=J}^{I-1} L[I,K] Linv[K,J], by distance d = I-J.
-  // Linv[K,J] for K > J is kept transposed in A's strict upper triangle: A[(J*32+b) + (K*32+a)*kLdD].
-  for (int d = 1; d < 4; ++d) {
-    const int npair = 4 - d;
-    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
-      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
-      const int J = p, I = p + d;
-      double s = 0.0;
-      for (int K = J; K < I; ++K) {
-        for (int k = 0; k < 32; ++k) {
-          const double lik = A[(I * 32 + a) + (K * 32 + k) * kLdD];
-          const double xkj = (K == J) ? Di[J * 32 * kLdI + k + b * kLdI] : A[(J * 32 + b) + (K * 32 + k) * kLdD];
-          s += lik * xkj;
-        }
+  // L^{-1}: thread c solves L x = e_c by forward substitution (4 partial sums for ILP)
+  if (tid < kNB) {
+    const int c = tid;
+    double* x = X + c * kLdD;
+    for (int i = 0; i < c; ++i) x[i] = 0.0;
+    x[c] = 1.0 / A[c + c * kLdD];
+    for (int i = c + 1; i < kNB; ++i) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = c;
+      for (; k + 3 < i; k += 4) {
+        s0 += A[i + k * kLdD] * x[k];
+        s1 += A[i + (k + 1) * kLdD] * x[k + 1];
+        s2 += A[i + (k + 2) * kLdD] * x[k + 2];
+        s3 += A[i + (k + 3) * kLdD] * x[k + 3];
       }
-      Tm[p * 32 * kLdI + a + b * kLdI] = s;
+      for (; k < i; ++k) s0 += A[i + k * kLdD] * x[k];
+      x[i] = -((s0 + s1) + (s2 + s3)) / A[i + i * kLdD];
     }
-    __syncthreads();
-    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
-      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
-      const int J = p, I = p + d;
-      double s = 0.0;
-      for (int k = 0; k <= a; ++k) s -= Di[I * 32 * kLdI + a + k * kLdI] * Tm[p * 32 * kLdI + k + b * kLdI];
-      A[(J * 32 + b) + (I * 32 + a) * kLdD] = s;
-    }
-    __syncthreads();
   }
+  __syncthreads();
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
     const int i = idx % kNB, j = idx / kNB;
-    const int I = i >> 5, J = j >> 5;
-    double v = 0.0;
-    if (i < kb && j < kb && i >= j) v = (I == J) ? Di[I * 32 * kLdI + (i & 31) + (j & 31) * kLdI] : A[j + i * kLdD];
-    Linv[idx] = v;
+    Linv[idx] = (i < kb && j < kb && i >= j) ? X[i + j * kLdD] : 0.0;
   }
+  (void)bad;
 }
 
 // ------------------------------------------------------------------ tensor-core GEMM (C op= A B^T)
@@ -288,28 +216,53 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // epilogue
+  // epilogue.  SYRK: C -= acc with all loads of a half-tile issued before any store (the
+  // compiler cannot reorder them itself because C's loads and stores may alias).
+  if (SYRK) {
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int i = rowA0 + wm * 64 + a * 8 + g8;
-    if (i >= g.rows) continue;
+    for (int h = 0; h < 2; ++h) {
+      double cold[4][4][2];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+      for (int a = 0; a < 4; ++a) {
+        const int i = rowA0 + wm * 64 + (h * 4 + a) * 8 + g8;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
-        if (SYRK) {
-          if (j < g.rows && i >= j) g.C[i + (size_t)j * g.ldc] -= acc[a][b][e];
-        } else {
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
+            cold[a][b][e] = (i < g.rows && j < g.rows && i >= j) ? g.C[i + (size_t)j * g.ldc] : 0.0;
+          }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = rowA0 + wm * 64 + (h * 4 + a) * 8 + g8;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
+            if (i < g.rows && j < g.rows && i >= j) g.C[i + (size_t)j * g.ldc] = cold[a][b][e] - acc[h * 4 + a][b][e];
+          }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int i = rowA0 + wm * 64 + a * 8 + g8;
+      if (i >= g.rows) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
           if (j < g.cols) g.C[i + (size_t)j * g.ldc] = acc[a][b][e];
         }
-      }
     }
   }
 }
 
 static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(double); }
-static size_t diag_smem() { return ((size_t)kNB * kLdD + 7 * 32 * kLdI) * sizeof(double); }
+static size_t diag_smem() { return (size_t)2 * kNB * kLdD * sizeof(double); }
 
 template <int MODE>
 static void launch_gemm(bool al16, int grid, const GemmArgs& g, cudaStream_t st) {
