@@ -37,8 +37,7 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
   extern __shared__ double sm[];
-  double* A = sm;                 // 128 x 128 (ld 129): lower = L
-  double* X = A + kNB * kLdD;     // 128 x 128 (ld 129): L^{-1}, column c owned by thread c
+  double* A = sm;                 // 128 x 128 (ld 129): lower = L, upper = L^{-T}
   __shared__ double col[2][kNB];  // scaled pivot column, double-buffered
   __shared__ int bad;
   const int tid = threadIdx.x;
@@ -80,29 +79,32 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
-  // L^{-1}: thread c solves L x = e_c by forward substitution (4 partial sums for ILP)
+  // L^{-1}: thread c solves L x = e_c by forward substitution (4 partial sums for ILP).  x is kept
+  // in row c of A's upper triangle (x[i] at A[c + i*ld], i >= c); L's diagonal moves to dL first.
+  __shared__ double dL[kNB];
+  for (int i = tid; i < kNB; i += kDiagThreads) dL[i] = A[i + i * kLdD];
+  __syncthreads();
   if (tid < kNB) {
     const int c = tid;
-    double* x = X + c * kLdD;
-    for (int i = 0; i < c; ++i) x[i] = 0.0;
-    x[c] = 1.0 / A[c + c * kLdD];
+    double* xr = A + c;  // x[i] = xr[i * kLdD]
+    xr[c * kLdD] = 1.0 / dL[c];
     for (int i = c + 1; i < kNB; ++i) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int k = c;
       for (; k + 3 < i; k += 4) {
-        s0 += A[i + k * kLdD] * x[k];
-        s1 += A[i + (k + 1) * kLdD] * x[k + 1];
-        s2 += A[i + (k + 2) * kLdD] * x[k + 2];
-        s3 += A[i + (k + 3) * kLdD] * x[k + 3];
+        s0 += A[i + k * kLdD] * xr[k * kLdD];
+        s1 += A[i + (k + 1) * kLdD] * xr[(k + 1) * kLdD];
+        s2 += A[i + (k + 2) * kLdD] * xr[(k + 2) * kLdD];
+        s3 += A[i + (k + 3) * kLdD] * xr[(k + 3) * kLdD];
       }
-      for (; k < i; ++k) s0 += A[i + k * kLdD] * x[k];
-      x[i] = -((s0 + s1) + (s2 + s3)) / A[i + i * kLdD];
+      for (; k < i; ++k) s0 += A[i + k * kLdD] * xr[k * kLdD];
+      xr[i * kLdD] = -((s0 + s1) + (s2 + s3)) / dL[i];
     }
   }
   __syncthreads();
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
     const int i = idx % kNB, j = idx / kNB;
-    Linv[idx] = (i < kb && j < kb && i >= j) ? X[i + j * kLdD] : 0.0;
+    Linv[idx] = (i < kb && j < kb && i >= j) ? A[j + i * kLdD] : 0.0;
   }
   (void)bad;
 }
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
 }
 
 static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(double); }
-static size_t diag_smem() { return (size_t)2 * kNB * kLdD * sizeof(double); }
+static size_t diag_smem() { return (size_t)kNB * kLdD * sizeof(double); }
 
 template <int MODE>
 static void launch_gemm(bool al16, int grid, const GemmArgs& g, cudaStream_t st) {

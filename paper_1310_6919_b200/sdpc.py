@@ -120,7 +120,8 @@ class Handle:
 
     def _check(self, st, where):
         if st != SDPC_OK:
-            raise SdpcError(st, lib().sdpc_last_info(self.h), where)
+            msg = lib().sdpc_last_error_message(self.h).decode()
+            raise SdpcError(st, lib().sdpc_last_info(self.h), where + (f" [{msg}]" if msg else ""))
 
     def get_structure(self):
         s = _Structure()
