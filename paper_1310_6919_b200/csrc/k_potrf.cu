@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
   if (tid == 0) bad = 0;
   __syncthreads();
   // right-looking unblocked Cholesky, the whole CTA per column (2 barriers per column)
+  const int lane = tid & 31, wid = tid >> 5;
   for (int j = 0; j < kNB; ++j) {
     const double d = A[j + j * kLdD];
     if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
@@ -60,18 +61,15 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     }
     const double r = rsqrt(d);
     double* cj = col[j & 1];
-    for (int i = j + tid; i < kNB; i += kDiagThreads) {
-      const double v = (i == j) ? d * r : A[i + j * kLdD] * r;
-      cj[i] = v;
-      A[i + j * kLdD] = v;
+    if (tid >= j && tid < kNB) {
+      const double v = (tid == j) ? d * r : A[tid + j * kLdD] * r;
+      cj[tid] = v;
+      A[tid + j * kLdD] = v;
     }
     __syncthreads();
-    const int nr = kNB - j - 1;
-    for (int idx = tid; idx < nr * nr; idx += kDiagThreads) {
-      const int ii = idx % nr, kk = idx / nr;
-      if (ii < kk) continue;
-      const int i = j + 1 + ii, k = j + 1 + kk;
-      A[i + k * kLdD] -= cj[i] * cj[k];
+    for (int k = j + 1 + wid; k < kNB; k += kDiagThreads / 32) {
+      const double ck = cj[k];
+      for (int i = k + lane; i < kNB; i += 32) A[i + k * kLdD] -= cj[i] * ck;
     }
     __syncthreads();
   }
@@ -79,29 +77,53 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
-  // L^{-1}: thread c solves L x = e_c by forward substitution (4 partial sums for ILP).  x is kept
-  // in row c of A's upper triangle (x[i] at A[c + i*ld], i >= c); L's diagonal moves to dL first.
+  // L^{-1}, kept transposed in A's upper triangle: Linv[i][j] at A[j + i*ld] (i >= j).
+  // (1) the four 32 x 32 diagonal blocks: thread (I, c) forward-substitutes column c of block I;
+  // (2) off-diagonal blocks by distance d = I - J: Linv[I,J] = -Linv[I,I] sum_{K=J}^{I-1} L[I,K] Linv[K,J].
   __shared__ double dL[kNB];
-  for (int i = tid; i < kNB; i += kDiagThreads) dL[i] = A[i + i * kLdD];
+  if (tid < kNB) dL[tid] = A[tid + tid * kLdD];
   __syncthreads();
   if (tid < kNB) {
-    const int c = tid;
-    double* xr = A + c;  // x[i] = xr[i * kLdD]
-    xr[c * kLdD] = 1.0 / dL[c];
-    for (int i = c + 1; i < kNB; ++i) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int I = tid >> 5, c = tid & 31, o = I * 32;
+    double* xr = A + (o + c);  // Linv[o+i][o+c] at xr[(o+i) * kLdD]
+    xr[(o + c) * kLdD] = 1.0 / dL[o + c];
+    for (int i = c + 1; i < 32; ++i) {
+      double s0 = 0.0, s1 = 0.0;
       int k = c;
-      for (; k + 3 < i; k += 4) {
-        s0 += A[i + k * kLdD] * xr[k * kLdD];
-        s1 += A[i + (k + 1) * kLdD] * xr[(k + 1) * kLdD];
-        s2 += A[i + (k + 2) * kLdD] * xr[(k + 2) * kLdD];
-        s3 += A[i + (k + 3) * kLdD] * xr[(k + 3) * kLdD];
+      for (; k + 1 < i; k += 2) {
+        s0 += A[(o + i) + (o + k) * kLdD] * xr[(o + k) * kLdD];
+        s1 += A[(o + i) + (o + k + 1) * kLdD] * xr[(o + k + 1) * kLdD];
       }
-      for (; k < i; ++k) s0 += A[i + k * kLdD] * xr[k * kLdD];
-      xr[i * kLdD] = -((s0 + s1) + (s2 + s3)) / dL[i];
+      if (k < i) s0 += A[(o + i) + (o + k) * kLdD] * xr[(o + k) * kLdD];
+      xr[(o + i) * kLdD] = -(s0 + s1) / dL[o + i];
     }
   }
   __syncthreads();
+  __shared__ double T[3][32][33];
+  for (int d = 1; d < 4; ++d) {
+    const int npair = 4 - d;
+    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
+      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
+      const int J = p, I = p + d;
+      double acc = 0.0;
+      // K == J: Linv[J,J] is lower, so only k >= b contributes (the rest of that storage is L)
+      for (int k = b; k < 32; ++k) acc += A[(I * 32 + a) + (J * 32 + k) * kLdD] * A[(J * 32 + b) + (J * 32 + k) * kLdD];
+      for (int K = J + 1; K < I; ++K)
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k)
+          acc += A[(I * 32 + a) + (K * 32 + k) * kLdD] * A[(J * 32 + b) + (K * 32 + k) * kLdD];
+      T[p][a][b] = acc;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
+      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
+      const int J = p, I = p + d;
+      double acc = 0.0;
+      for (int k = 0; k <= a; ++k) acc -= A[(I * 32 + k) + (I * 32 + a) * kLdD] * T[p][k][b];
+      A[(J * 32 + b) + (I * 32 + a) * kLdD] = acc;
+    }
+    __syncthreads();
+  }
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
     const int i = idx % kNB, j = idx / kNB;
     Linv[idx] = (i < kb && j < kb && i >= j) ? A[j + i * kLdD] : 0.0;
