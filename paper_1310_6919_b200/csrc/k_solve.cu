@@ -4,13 +4,15 @@
 // PAPER.md P:320-330 (forward/backward substitution instead of forming X-hat),
 // P:686-688 (Eq. newSCM2: x_p = L-hat^{-T} L-hat^{-1} e_p, v = N^{-T} N^{-1} [A_j]_{*k}),
 // P:859-869 (reuse of x_p across a column of B; on B200 the whole X-hat fits in HBM, so the
-// columns are materialised once and reused by every column of B, SURVEY §8(a) notes).
+// columns are materialised once and reused by every column of B, reading #21).
 //
 // Per panel P (columns p0 = 32P .. p0+31, elimination order):
 //   forward  L z = E_P  over the union of the etree paths of the panel's columns (ascending
-//            supernodes; rows outside the paths are exactly zero);  z <- D^{-1} z;
-//   backward L^T x = z  over all supernodes, level by level from the roots (no write conflicts:
-//            a supernode writes only its own rows S_r and reads ancestors U_r).
+//            supernodes, whole CTA per supernode; rows off the paths are exactly zero); z <- D^{-1} z;
+//   backward L^T x = z  over all supernodes, level by level from the roots, one warp per supernode
+//            (no write conflicts: a supernode writes only its rows S_r and reads ancestors' rows U_r).
+// Both sweeps keep up to 16 columns of a supernode in registers, so every row x[U_q] is read once
+// per 16 columns (not once per column).
 // Output layout: panel-major, X[P][i][lane] (row i of the panel = 32 contiguous doubles).
 #include <cuda_runtime.h>
 
@@ -37,6 +39,45 @@ struct SolveArgs {
 };
 
 constexpr int kSolveThreads = 256;
+constexpr int kCh = 16;  // register chunk of supernode columns
+
+__device__ __forceinline__ double& xrow(double* X, int row, int lane) { return X[(size_t)row * kPanelW + lane]; }
+
+// backward for one supernode, one warp: x[S] = L_SS^{-T} (y[S] - L_US^T x[U])
+__device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int c, int s, int f,
+                                              const int32_t* __restrict__ U, double* X, int lane, bool onpath) {
+  const int u = c - s;
+  for (int t1 = s; t1 > 0; t1 -= kCh) {
+    const int t0 = t1 > kCh ? t1 - kCh : 0;
+    const int w = t1 - t0;
+    double acc[kCh];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) acc[j] = (j < w && onpath) ? xrow(X, f + t0 + j, lane) : 0.0;
+    const double* Lc = Lr + (size_t)t0 * c;  // Lc[i + j*c] = L[i, t0+j]
+#pragma unroll 2
+    for (int q = 0; q < u; ++q) {
+      const double xq = xrow(X, U[q], lane);
+#pragma unroll
+      for (int j = 0; j < kCh; ++j)
+        if (j < w) acc[j] -= Lc[s + q + (size_t)j * c] * xq;
+    }
+    for (int tp = t1; tp < s; ++tp) {
+      const double xq = xrow(X, f + tp, lane);
+#pragma unroll
+      for (int j = 0; j < kCh; ++j)
+        if (j < w) acc[j] -= Lc[tp + (size_t)j * c] * xq;
+    }
+#pragma unroll
+    for (int j = kCh - 1; j >= 0; --j) {
+      if (j < w) {
+        const double xj = acc[j];
+        xrow(X, f + t0 + j, lane) = xj;
+#pragma unroll
+        for (int jj = 0; jj < j; ++jj) acc[jj] -= Lc[(t0 + j) + (size_t)jj * c] * xj;
+      }
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ uint32_t inreach[];  // bitmap over supernodes
@@ -58,12 +99,11 @@ __global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs 
     const int r = a.reach_sn[q];
     atomicOr(&inreach[r >> 5], 1u << (r & 31));
   }
-  __syncthreads();
   // initialise z rows on the paths: z[i][lane] = (i == p0 + lane)
   for (int q = rb + wid; q < re; q += NW) {
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r];
-    for (int t = 0; t < s; ++t) X[(size_t)(f + t) * kPanelW + lane] = (f + t == p0 + lane) ? 1.0 : 0.0;
+    for (int t = 0; t < s; ++t) xrow(X, f + t, lane) = (f + t == p0 + lane) ? 1.0 : 0.0;
   }
   __syncthreads();
 
@@ -72,23 +112,50 @@ __global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs 
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
     const double* Lr = Lp + a.panel_off[r];
-    if (wid == 0) {  // unit lower diagonal block
-      for (int t = 1; t < s; ++t) {
-        double acc = X[(size_t)(f + t) * kPanelW + lane];
-        for (int tp = 0; tp < t; ++tp) acc -= Lr[t + (size_t)tp * c] * X[(size_t)(f + tp) * kPanelW + lane];
-        X[(size_t)(f + t) * kPanelW + lane] = acc;
+    if (wid == 0) {  // unit lower diagonal block, register chunks of kCh rows
+      for (int t0 = 0; t0 < s; t0 += kCh) {
+        const int w = min(kCh, s - t0);
+        double acc[kCh];
+#pragma unroll
+        for (int j = 0; j < kCh; ++j) acc[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
+        for (int tp = 0; tp < t0; ++tp) {
+          const double zt = xrow(X, f + tp, lane);
+#pragma unroll
+          for (int j = 0; j < kCh; ++j)
+            if (j < w) acc[j] -= Lr[(t0 + j) + (size_t)tp * c] * zt;
+        }
+#pragma unroll
+        for (int j = 0; j < kCh; ++j) {
+          if (j < w) {
+            const double zj = acc[j];
+            xrow(X, f + t0 + j, lane) = zj;
+#pragma unroll
+            for (int jj = j + 1; jj < kCh; ++jj)
+              if (jj < w) acc[jj] -= Lr[(t0 + jj) + (size_t)(t0 + j) * c] * zj;
+          }
+        }
       }
     }
     __syncthreads();
-    const int32_t* U = rowind + a.colptr[f] + s;
-    for (int qq = wid; qq < u; qq += NW) {
-      const int row = U[qq];
-      double acc = X[(size_t)row * kPanelW + lane];
-      for (int t = 0; t < s; ++t) acc -= Lr[s + qq + (size_t)t * c] * X[(size_t)(f + t) * kPanelW + lane];
-      X[(size_t)row * kPanelW + lane] = acc;
+    if (u > 0) {
+      const int32_t* U = rowind + a.colptr[f] + s;
+      for (int t0 = 0; t0 < s; t0 += kCh) {
+        const int w = min(kCh, s - t0);
+        double zt[kCh];
+#pragma unroll
+        for (int j = 0; j < kCh; ++j) zt[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
+        const double* Lc = Lr + (size_t)t0 * c;
+        for (int qq = wid; qq < u; qq += NW) {
+          double acc = xrow(X, U[qq], lane);
+#pragma unroll
+          for (int j = 0; j < kCh; ++j)
+            if (j < w) acc -= Lc[s + qq + (size_t)j * c] * zt[j];
+          xrow(X, U[qq], lane) = acc;
+        }
+      }
     }
     __syncthreads();
-    for (int t = wid; t < s; t += NW) X[(size_t)(f + t) * kPanelW + lane] /= D[f + t];
+    for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) /= D[f + t];
   }
   __syncthreads();
 
@@ -96,17 +163,9 @@ __global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs 
   for (int lv = 0; lv < a.ndlev; ++lv) {
     for (int q = a.dlev_ptr[lv] + wid; q < a.dlev_ptr[lv + 1]; q += NW) {
       const int r = a.dlev_sn[q];
-      const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
+      const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
       const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
-      const double* Lr = Lp + a.panel_off[r];
-      const int32_t* U = rowind + a.colptr[f] + s;
-      for (int t = s - 1; t >= 0; --t) {
-        double acc = onpath ? X[(size_t)(f + t) * kPanelW + lane] : 0.0;
-        const double* Lc = Lr + (size_t)t * c;
-        for (int qq = 0; qq < u; ++qq) acc -= Lc[s + qq] * X[(size_t)U[qq] * kPanelW + lane];
-        for (int tp = t + 1; tp < s; ++tp) acc -= Lc[tp] * X[(size_t)(f + tp) * kPanelW + lane];
-        X[(size_t)(f + t) * kPanelW + lane] = acc;
-      }
+      bwd_supernode(Lp + a.panel_off[r], c, s, f, rowind + a.colptr[f] + s, X, lane, onpath);
     }
     __syncthreads();
   }

@@ -259,6 +259,15 @@ std::string analyse(Symbolic& S, int32_t n, int32_t m, const int64_t* a_ptr, con
   };
   group(S.height, S.hlev_ptr, S.hlev_sn);
   group(S.depth, S.dlev_ptr, S.dlev_sn);
+  // within a depth level, the most work first (backward solve: one warp per supernode)
+  for (size_t lv = 0; lv + 1 < S.dlev_ptr.size(); ++lv) {
+    auto b = S.dlev_sn.begin() + S.dlev_ptr[lv], e = S.dlev_sn.begin() + S.dlev_ptr[lv + 1];
+    std::stable_sort(b, e, [&](int32_t x, int32_t y) {
+      const int64_t wx = (int64_t)S.sns[x] * (S.snc[x] - S.sns[x]) + (int64_t)S.sns[x] * S.sns[x] / 2;
+      const int64_t wy = (int64_t)S.sns[y] * (S.snc[y] - S.sns[y]) + (int64_t)S.sns[y] * S.sns[y] / 2;
+      return wx > wy;
+    });
+  }
   return "";
 }
 
