@@ -51,25 +51,63 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
   }
   if (tid == 0) bad = 0;
   __syncthreads();
-  // right-looking unblocked Cholesky, the whole CTA per column (2 barriers per column)
-  const int lane = tid & 31, wid = tid >> 5;
-  for (int j = 0; j < kNB; ++j) {
-    const double d = A[j + j * kLdD];
-    if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
-      if (tid == 0) report_error(err, k0 + j + 1);
-      return;
+  // blocked right-looking Cholesky: 32-column panels factored column by column by the whole CTA
+  // (thread = row, independent updates of the panel's remaining columns), then one 4 x 4
+  // register-tiled trailing update per panel.
+  for (int jb = 0; jb < kNB; jb += 32) {
+    for (int j = jb; j < jb + 32; ++j) {
+      const double d = A[j + j * kLdD];
+      if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
+        if (tid == 0) report_error(err, k0 + j + 1);
+        return;
+      }
+      const double r = rsqrt(d);
+      double* cj = col[j & 1];
+      if (tid >= j && tid < kNB) {
+        const double v = (tid == j) ? d * r : A[tid + j * kLdD] * r;
+        cj[tid] = v;
+        A[tid + j * kLdD] = v;
+      }
+      __syncthreads();
+      // columns k in (j, jb+32), rows i >= k: thread (i = tid % 128, half = tid / 128)
+      const int i = tid & (kNB - 1), half = tid >> 7;
+      if (i > j) {
+        const double ci = cj[i];
+        for (int k = j + 1 + half; k < jb + 32 && k <= i; k += 2) A[i + k * kLdD] -= ci * cj[k];
+      }
+      __syncthreads();
     }
-    const double r = rsqrt(d);
-    double* cj = col[j & 1];
-    if (tid >= j && tid < kNB) {
-      const double v = (tid == j) ? d * r : A[tid + j * kLdD] * r;
-      cj[tid] = v;
-      A[tid + j * kLdD] = v;
-    }
-    __syncthreads();
-    for (int k = j + 1 + wid; k < kNB; k += kDiagThreads / 32) {
-      const double ck = cj[k];
-      for (int i = k + lane; i < kNB; i += 32) A[i + k * kLdD] -= cj[i] * ck;
+    // trailing update of rows/cols >= jb+32 with the panel columns jb..jb+31
+    const int r0 = jb + 32, nr = kNB - r0;
+    if (nr > 0) {
+      const int nb4 = nr / 4;  // nr is a multiple of 32
+      const int ntile = nb4 * (nb4 + 1) / 2;
+      for (int t = tid; t < ntile; t += kDiagThreads) {
+        int bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while (bi * (bi + 1) / 2 > t) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+        const int bj = t - bi * (bi + 1) / 2;
+        const int i0 = r0 + 4 * bi, j0 = r0 + 4 * bj;
+        double acc[4][4] = {};
+#pragma unroll 4
+        for (int k = jb; k < jb + 32; ++k) {
+          double pi[4], pj[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            pi[q] = A[i0 + q + k * kLdD];
+            pj[q] = A[j0 + q + k * kLdD];
+          }
+#pragma unroll
+          for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+            for (int b2 = 0; b2 < 4; ++b2) acc[a2][b2] += pi[a2] * pj[b2];
+        }
+#pragma unroll
+        for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2)
+            if (i0 + a2 >= j0 + b2) A[(i0 + a2) + (j0 + b2) * kLdD] -= acc[a2][b2];
+      }
     }
     __syncthreads();
   }

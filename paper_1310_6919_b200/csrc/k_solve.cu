@@ -39,11 +39,12 @@ struct SolveArgs {
 };
 
 constexpr int kSolveThreads = 256;
-constexpr int kCh = 16;  // register chunk of supernode columns
+constexpr int kCh = 16;  // register chunk of supernode columns (widest instantiation)
 
 __device__ __forceinline__ double& xrow(double* X, int row, int lane) { return X[(size_t)row * kPanelW + lane]; }
 
-// backward for one supernode, one warp: x[S] = L_SS^{-T} (y[S] - L_US^T x[U])
+// backward for one supernode, one warp: x[S] = L_SS^{-T} (y[S] - L_US^T x[U]); CH = register chunk
+template <int kCh>
 __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int c, int s, int f,
                                               const int32_t* __restrict__ U, double* X, int lane, bool onpath) {
   const int u = c - s;
@@ -79,7 +80,28 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs a) {
+// forward update of the U rows of one supernode by all warps: x[U] -= L_US z[S] (S rows final)
+template <int kCh>
+__device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c, int s, int f,
+                                           const int32_t* __restrict__ U, double* X, int lane, int wid, int nw) {
+  const int u = c - s;
+  for (int t0 = 0; t0 < s; t0 += kCh) {
+    const int w = min(kCh, s - t0);
+    double zt[kCh];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) zt[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
+    const double* Lc = Lr + (size_t)t0 * c;
+    for (int qq = wid; qq < u; qq += nw) {
+      double acc = xrow(X, U[qq], lane);
+#pragma unroll
+      for (int j = 0; j < kCh; ++j)
+        if (j < w) acc -= Lc[s + qq + (size_t)j * c] * zt[j];
+      xrow(X, U[qq], lane) = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ uint32_t inreach[];  // bitmap over supernodes
   const int P = blockIdx.x, fac = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -139,20 +161,11 @@ __global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs 
     __syncthreads();
     if (u > 0) {
       const int32_t* U = rowind + a.colptr[f] + s;
-      for (int t0 = 0; t0 < s; t0 += kCh) {
-        const int w = min(kCh, s - t0);
-        double zt[kCh];
-#pragma unroll
-        for (int j = 0; j < kCh; ++j) zt[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
-        const double* Lc = Lr + (size_t)t0 * c;
-        for (int qq = wid; qq < u; qq += NW) {
-          double acc = xrow(X, U[qq], lane);
-#pragma unroll
-          for (int j = 0; j < kCh; ++j)
-            if (j < w) acc -= Lc[s + qq + (size_t)j * c] * zt[j];
-          xrow(X, U[qq], lane) = acc;
-        }
-      }
+      if (s <= 1) fwd_update<1>(Lr, c, s, f, U, X, lane, wid, NW);
+      else if (s <= 2) fwd_update<2>(Lr, c, s, f, U, X, lane, wid, NW);
+      else if (s <= 4) fwd_update<4>(Lr, c, s, f, U, X, lane, wid, NW);
+      else if (s <= 8) fwd_update<8>(Lr, c, s, f, U, X, lane, wid, NW);
+      else fwd_update<16>(Lr, c, s, f, U, X, lane, wid, NW);
     }
     __syncthreads();
     for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) /= D[f + t];
@@ -165,7 +178,13 @@ __global__ void __launch_bounds__(kSolveThreads) inverse_panel_kernel(SolveArgs 
       const int r = a.dlev_sn[q];
       const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
       const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
-      bwd_supernode(Lp + a.panel_off[r], c, s, f, rowind + a.colptr[f] + s, X, lane, onpath);
+      const double* Lr = Lp + a.panel_off[r];
+      const int32_t* U = rowind + a.colptr[f] + s;
+      if (s <= 1) bwd_supernode<1>(Lr, c, s, f, U, X, lane, onpath);
+      else if (s <= 2) bwd_supernode<2>(Lr, c, s, f, U, X, lane, onpath);
+      else if (s <= 4) bwd_supernode<4>(Lr, c, s, f, U, X, lane, onpath);
+      else if (s <= 8) bwd_supernode<8>(Lr, c, s, f, U, X, lane, onpath);
+      else bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
     }
     __syncthreads();
   }
