@@ -2,8 +2,9 @@
 // PAPER.md P:711-713 / P:735-736 / P:978-979 (type (i): LAPACK dense Cholesky with multithreaded BLAS).
 //
 // Blocked right-looking, nb = 128, with depth-1 lookahead on a second stream.  Per panel step k:
-//   diag(k)   : one CTA factors the 128 x 128 diagonal block in shared memory (whole CTA per
-//               column, two barriers per column) and forms L11^{-1} (thread per column) for the TRSM;
+//   diag(k)   : one CTA (512 threads) factors the 128 x 128 diagonal block in shared memory
+//               (32-column panels, one barrier per column, register-tiled panel updates) and forms
+//               L11^{-1} (blocked by 32) for the TRSM;
 //   trsm(k)   : L21 = A21 L11^{-T} as an FP64 tensor-core GEMM with the explicit inverse;
 //   ucol(k)   : trailing update of block column k+1 only (one column of 128 x 128 tiles);
 //   diag(k+1), trsm(k+1) run on the side stream while
@@ -30,16 +31,17 @@ constexpr int kLdS = kTile + 4;  // smem row stride (doubles): conflict-free fra
 constexpr int kGemmThreads = 256;
 
 // ------------------------------------------------------------------ diagonal block
-constexpr int kDiagThreads = 256;
+constexpr int kDiagThreads = 512;
 constexpr int kLdD = kNB + 1;  // A[i + j*kLdD]
 
 __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
   extern __shared__ double sm[];
-  double* A = sm;                 // 128 x 128 (ld 129): lower = L, upper = L^{-T}
-  __shared__ double col[2][kNB];  // scaled pivot column, double-buffered
-  __shared__ int bad;
+  double* A = sm;                  // 128 x 128 (ld 129): lower = L, upper = L^{-T}
+  __shared__ double P[32][kNB];    // current 32-column panel, scaled (P[k][i] = L[i, jb+k])
+  __shared__ double dL[kNB];
+  __shared__ double T[3][32][33];
   const int tid = threadIdx.x;
   double* Bd = B + k0 + (size_t)k0 * ld;
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
@@ -49,38 +51,39 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     else if (i == j) v = 1.0;  // identity padding beyond kb
     A[i + j * kLdD] = v;
   }
-  if (tid == 0) bad = 0;
   __syncthreads();
-  // blocked right-looking Cholesky: 32-column panels factored column by column by the whole CTA
-  // (thread = row, independent updates of the panel's remaining columns), then one 4 x 4
-  // register-tiled trailing update per panel.
+  const int row = tid & (kNB - 1), slice = tid >> 7;  // 4 slices of 8 columns
   for (int jb = 0; jb < kNB; jb += 32) {
+    // column by column inside the panel, one barrier per column: the update uses the unscaled
+    // column j (A[i,k] -= A[i,j] A[k,j] / d); the scaled column goes to P.
     for (int j = jb; j < jb + 32; ++j) {
       const double d = A[j + j * kLdD];
       if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
         if (tid == 0) report_error(err, k0 + j + 1);
         return;
       }
-      const double r = rsqrt(d);
-      double* cj = col[j & 1];
-      if (tid >= j && tid < kNB) {
-        const double v = (tid == j) ? d * r : A[tid + j * kLdD] * r;
-        cj[tid] = v;
-        A[tid + j * kLdD] = v;
-      }
-      __syncthreads();
-      // columns k in (j, jb+32), rows i >= k: thread (i = tid % 128, half = tid / 128)
-      const int i = tid & (kNB - 1), half = tid >> 7;
-      if (i > j) {
-        const double ci = cj[i];
-        for (int k = j + 1 + half; k < jb + 32 && k <= i; k += 2) A[i + k * kLdD] -= ci * cj[k];
+      const double inv_d = 1.0 / d;
+      const double aij = (row >= j) ? A[row + j * kLdD] : 0.0;
+      if (slice == 0 && row >= j) P[j - jb][row] = aij * rsqrt(d);
+      if (row > j) {
+        const double fi = aij * inv_d;
+        const int kbeg = jb + slice * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int k = kbeg + q;
+          if (k > j && k <= row) A[row + k * kLdD] -= fi * A[k + j * kLdD];
+        }
       }
       __syncthreads();
     }
-    // trailing update of rows/cols >= jb+32 with the panel columns jb..jb+31
+    for (int idx = tid; idx < 32 * kNB; idx += kDiagThreads) {
+      const int k = idx >> 7, i = idx & (kNB - 1);
+      if (i >= jb + k) A[i + (jb + k) * kLdD] = P[k][i];
+    }
+    // trailing update of rows/cols >= jb+32 with the panel: 4 x 4 register tiles
     const int r0 = jb + 32, nr = kNB - r0;
     if (nr > 0) {
-      const int nb4 = nr / 4;  // nr is a multiple of 32
+      const int nb4 = nr / 4;
       const int ntile = nb4 * (nb4 + 1) / 2;
       for (int t = tid; t < ntile; t += kDiagThreads) {
         int bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
@@ -89,13 +92,13 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
         const int bj = t - bi * (bi + 1) / 2;
         const int i0 = r0 + 4 * bi, j0 = r0 + 4 * bj;
         double acc[4][4] = {};
-#pragma unroll 4
-        for (int k = jb; k < jb + 32; ++k) {
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
           double pi[4], pj[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            pi[q] = A[i0 + q + k * kLdD];
-            pj[q] = A[j0 + q + k * kLdD];
+            pi[q] = P[k][i0 + q];
+            pj[q] = P[k][j0 + q];
           }
 #pragma unroll
           for (int a2 = 0; a2 < 4; ++a2)
@@ -118,7 +121,6 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
   // L^{-1}, kept transposed in A's upper triangle: Linv[i][j] at A[j + i*ld] (i >= j).
   // (1) the four 32 x 32 diagonal blocks: thread (I, c) forward-substitutes column c of block I;
   // (2) off-diagonal blocks by distance d = I - J: Linv[I,J] = -Linv[I,I] sum_{K=J}^{I-1} L[I,K] Linv[K,J].
-  __shared__ double dL[kNB];
   if (tid < kNB) dL[tid] = A[tid + tid * kLdD];
   __syncthreads();
   if (tid < kNB) {
@@ -137,20 +139,21 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     }
   }
   __syncthreads();
-  __shared__ double T[3][32][33];
   for (int d = 1; d < 4; ++d) {
     const int npair = 4 - d;
     for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
       const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
       const int J = p, I = p + d;
-      double acc = 0.0;
+      double acc0 = 0.0, acc1 = 0.0;
       // K == J: Linv[J,J] is lower, so only k >= b contributes (the rest of that storage is L)
-      for (int k = b; k < 32; ++k) acc += A[(I * 32 + a) + (J * 32 + k) * kLdD] * A[(J * 32 + b) + (J * 32 + k) * kLdD];
+      for (int k = b; k < 32; ++k) acc0 += A[(I * 32 + a) + (J * 32 + k) * kLdD] * A[(J * 32 + b) + (J * 32 + k) * kLdD];
       for (int K = J + 1; K < I; ++K)
 #pragma unroll 8
-        for (int k = 0; k < 32; ++k)
-          acc += A[(I * 32 + a) + (K * 32 + k) * kLdD] * A[(J * 32 + b) + (K * 32 + k) * kLdD];
-      T[p][a][b] = acc;
+        for (int k = 0; k < 32; k += 2) {
+          acc0 += A[(I * 32 + a) + (K * 32 + k) * kLdD] * A[(J * 32 + b) + (K * 32 + k) * kLdD];
+          acc1 += A[(I * 32 + a) + (K * 32 + k + 1) * kLdD] * A[(J * 32 + b) + (K * 32 + k + 1) * kLdD];
+        }
+      T[p][a][b] = acc0 + acc1;
     }
     __syncthreads();
     for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
@@ -166,7 +169,6 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     const int i = idx % kNB, j = idx / kNB;
     Linv[idx] = (i < kb && j < kb && i >= j) ? A[j + i * kLdD] : 0.0;
   }
-  (void)bad;
 }
 
 // ------------------------------------------------------------------ tensor-core GEMM (C op= A B^T)

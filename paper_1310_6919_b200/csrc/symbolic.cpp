@@ -259,6 +259,19 @@ std::string analyse(Symbolic& S, int32_t n, int32_t m, const int64_t* a_ptr, con
   };
   group(S.height, S.hlev_ptr, S.hlev_sn);
   group(S.depth, S.dlev_ptr, S.dlev_sn);
+  // preorder of the supernodal forest (roots in index order, children in index order)
+  S.preorder.clear();
+  {
+    std::vector<int32_t> stack;
+    for (int32_t r = ns - 1; r >= 0; --r)
+      if (S.sparent[r] < 0) stack.push_back(r);
+    while (!stack.empty()) {
+      int32_t r = stack.back();
+      stack.pop_back();
+      S.preorder.push_back(r);
+      for (int32_t q = S.child_ptr[r + 1] - 1; q >= S.child_ptr[r]; --q) stack.push_back(S.child_list[q]);
+    }
+  }
   // within a depth level, the most work first (backward solve: one warp per supernode)
   for (size_t lv = 0; lv + 1 < S.dlev_ptr.size(); ++lv) {
     auto b = S.dlev_sn.begin() + S.dlev_ptr[lv], e = S.dlev_sn.begin() + S.dlev_ptr[lv + 1];

@@ -46,6 +46,7 @@ struct Symbolic {
   std::vector<int32_t> hlev_ptr, hlev_sn;  // supernodes grouped by height (for (a2))
   std::vector<int32_t> depth;            // per supernode, roots = 0
   std::vector<int32_t> dlev_ptr, dlev_sn;  // grouped by depth (backward solve)
+  std::vector<int32_t> preorder;           // supernodes, parents before children, subtrees contiguous
 
   int64_t nnzE() const { return colptr.empty() ? 0 : colptr.back(); }
 };
