@@ -39,9 +39,10 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
   if (*err != kNoError) return;
   extern __shared__ double sm[];
   double* A = sm;                  // 128 x 128 (ld 129): lower = L, upper = L^{-T}
-  __shared__ double P[32][kNB];    // current 32-column panel, scaled (P[k][i] = L[i, jb+k])
+  // current 32-column panel, scaled (P[k][i] = L[i, jb+k]), and scratch for the inverse blocks
+  double (*P)[kNB] = reinterpret_cast<double (*)[kNB]>(sm + kNB * kLdD);
+  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(sm + kNB * kLdD + 32 * kNB);
   __shared__ double dL[kNB];
-  __shared__ double T[3][32][33];
   const int tid = threadIdx.x;
   double* Bd = B + k0 + (size_t)k0 * ld;
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
 }
 
 static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(double); }
-static size_t diag_smem() { return (size_t)kNB * kLdD * sizeof(double); }
+static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kNB + 3 * 32 * 33) * sizeof(double); }
 
 template <int MODE>
 static void launch_gemm(bool al16, int grid, const GemmArgs& g, cudaStream_t st) {
