@@ -284,6 +284,8 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(d.dlev_ptr, S.dlev_ptr);
   UP(d.dlev_sn, S.dlev_sn);
   UP(d.preorder, S.preorder);
+  UP(d.border, S.border);
+  UP(d.sub_ptr, S.sub_ptr);
   UP(d.perm, S.perm);
   UP(d.iperm, S.iperm);
   UP(d.reach_ptr, reach_ptr);
@@ -329,7 +331,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   DevSym& d = h->d;
   void* ptrs[] = {d.colptr, d.rowind, d.super_ptr, d.snc, d.sns, d.sparent, d.panel_off, d.e2p, d.umap_off,
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
-                  d.dlev_ptr, d.dlev_sn, d.preorder, d.perm, d.iperm, d.reach_ptr, d.reach_sn, h->d_ws_off,
+                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, h->d_ws_off,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
                   h->d_err, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};

@@ -33,6 +33,8 @@ struct DevSym {
   int32_t* dlev_ptr = nullptr;  // depth level pointers (device copy)
   int32_t* dlev_sn = nullptr;
   int32_t* preorder = nullptr;
+  int32_t* border = nullptr;
+  int32_t* sub_ptr = nullptr;
   int32_t* perm = nullptr;
   int32_t* iperm = nullptr;
   int32_t* reach_ptr = nullptr;  // per RHS panel: supernodes on the union of etree paths

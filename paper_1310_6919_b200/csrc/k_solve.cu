@@ -9,9 +9,10 @@
 // Per panel P (columns p0 = 32P .. p0+31, elimination order):
 //   forward  L z = E_P  over the union of the etree paths of the panel's columns (ascending
 //            supernodes, whole CTA per supernode; rows off the paths are exactly zero); z <- D^{-1} z;
-//   backward L^T x = z  over all supernodes, one warp per supernode, dataflow in preorder: a warp
-//            starts a supernode as soon as its parent is done (no write conflicts: a supernode writes
-//            only its rows S_r and reads ancestors' rows U_r).
+//   backward L^T x = z  over all supernodes, one warp per task, dataflow: the top of the tree one
+//            supernode per task in level order, then whole bottom subtrees per warp in preorder; a task
+//            starts when its parent is done (no write conflicts: a supernode writes only its rows S_r
+//            and reads ancestors' rows U_r).
 // Both sweeps keep up to 16 columns of a supernode in registers, so every row x[U_q] is read once
 // per 16 columns (not once per column).
 // Output layout: panel-major, X[P][i][lane] (row i of the panel = 32 contiguous doubles).
@@ -34,7 +35,9 @@ struct SolveArgs {
   const int32_t* reach_sn;
   const int32_t* dlev_ptr;
   const int32_t* dlev_sn;
-  const int32_t* preorder;
+  const int32_t* border;   // backward task order: top supernodes (level order), then subtrees (preorder)
+  const int32_t* sub_ptr;  // [nsub+1] offsets of the subtrees in border (starting at ntop)
+  int32_t ntop, nsub;
   const int32_t* sparent;
   const double* Lp[2];
   const double* D[2];
@@ -175,39 +178,55 @@ __global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveAr
   }
   __syncthreads();
 
-  // backward L^T x = z, dataflow over supernodes: warps claim supernodes in preorder (parents
-  // first) from a shared counter and wait only for their parent's done flag.  Rows off the paths
+  // backward L^T x = z, dataflow: tasks are (a) single supernodes of the top of the tree, claimed
+  // in level order, each waiting for its parent's done flag, then (b) whole bottom subtrees, each
+  // processed by one warp in preorder (parents' rows are reused immediately).  Rows off the paths
   // have z = 0.
   uint32_t* done = inreach + nwords;
   for (int i = tid; i < nwords; i += kSolveThreads) done[i] = 0;
-  if (tid == 0) *(volatile int*)(done + nwords) = 0;
-  __syncthreads();
   int* ctr = reinterpret_cast<int*>(done + nwords);
-  const int ns = a.nsuper;
+  if (tid == 0) *ctr = 0;
+  __syncthreads();
+  const int ntask = a.ntop + a.nsub;
   for (;;) {
     int q = 0;
     if (lane == 0) q = atomicAdd(ctr, 1);
     q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= ns) break;
-    const int r = a.preorder[q];
-    const int pr = a.sparent[r];
-    if (pr >= 0) {
-      volatile uint32_t* dv = done;
-      while (((dv[pr >> 5] >> (pr & 31)) & 1u) == 0) __nanosleep(32);
-      __threadfence_block();
+    if (q >= ntask) break;
+    int b, e;
+    if (q < a.ntop) {
+      b = q;
+      e = q + 1;
+    } else {
+      b = a.sub_ptr[q - a.ntop];
+      e = a.sub_ptr[q - a.ntop + 1];
     }
-    const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
-    const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
-    const double* Lr = Lp + a.panel_off[r];
-    const int32_t* U = rowind + a.colptr[f] + s;
-    if (s <= 1) bwd_supernode<1>(Lr, c, s, f, U, X, lane, onpath);
-    else if (s <= 2) bwd_supernode<2>(Lr, c, s, f, U, X, lane, onpath);
-    else if (s <= 4) bwd_supernode<4>(Lr, c, s, f, U, X, lane, onpath);
-    else if (s <= 8) bwd_supernode<8>(Lr, c, s, f, U, X, lane, onpath);
-    else bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) atomicOr(&done[r >> 5], 1u << (r & 31));
+    {  // wait for the parent of the first node (top node or subtree root)
+      const int pr = a.sparent[a.border[b]];
+      if (pr >= 0) {
+        volatile uint32_t* dv = done;
+        while (((dv[pr >> 5] >> (pr & 31)) & 1u) == 0) __nanosleep(20);
+        __threadfence_block();
+      }
+    }
+    for (int it = b; it < e; ++it) {
+      const int r = a.border[it];
+      const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
+      const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
+      const double* Lr = Lp + a.panel_off[r];
+      const int32_t* U = rowind + a.colptr[f] + s;
+      if (s <= 1) bwd_supernode<1>(Lr, c, s, f, U, X, lane, onpath);
+      else if (s <= 2) bwd_supernode<2>(Lr, c, s, f, U, X, lane, onpath);
+      else if (s <= 4) bwd_supernode<4>(Lr, c, s, f, U, X, lane, onpath);
+      else if (s <= 8) bwd_supernode<8>(Lr, c, s, f, U, X, lane, onpath);
+      else bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
+    }
+    if (q < a.ntop) {
+      __threadfence_block();
+      __syncwarp();
+      const int r = a.border[b];
+      if (lane == 0) atomicOr(&done[r >> 5], 1u << (r & 31));
+    }
   }
 }
 
@@ -226,7 +245,10 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.reach_sn = h->d.reach_sn;
   a.dlev_ptr = h->d.dlev_ptr;
   a.dlev_sn = h->d.dlev_sn;
-  a.preorder = h->d.preorder;
+  a.border = h->d.border;
+  a.sub_ptr = h->d.sub_ptr;
+  a.ntop = h->S.ntop;
+  a.nsub = (int32_t)h->S.sub_ptr.size() - 1;
   a.sparent = h->d.sparent;
   a.Lp[0] = h->Lx;
   a.Lp[1] = h->Ly;

@@ -272,6 +272,49 @@ std::string analyse(Symbolic& S, int32_t n, int32_t m, const int64_t* a_ptr, con
       for (int32_t q = S.child_ptr[r + 1] - 1; q >= S.child_ptr[r]; --q) stack.push_back(S.child_list[q]);
     }
   }
+  // backward task decomposition: subtree work w(r) = sum over the subtree of s*u + s^2/2.
+  // Subtree roots: w(r) <= wmax < w(parent).  Everything above is "top".
+  {
+    std::vector<int64_t> w(ns, 0);
+    for (int32_t r = 0; r < ns; ++r) {
+      w[r] += (int64_t)S.sns[r] * (S.snc[r] - S.sns[r]) + (int64_t)S.sns[r] * (S.sns[r] + 1) / 2;
+      if (S.sparent[r] >= 0) w[S.sparent[r]] += w[r];
+    }
+    int64_t total = 0;
+    for (int32_t r = 0; r < ns; ++r)
+      if (S.sparent[r] < 0) total += w[r];
+    const int64_t wmax = std::max<int64_t>(1, total / 96);
+    std::vector<char> is_top(ns, 0);
+    std::vector<int32_t> roots;
+    for (int32_t r = 0; r < ns; ++r) {
+      const int32_t p = S.sparent[r];
+      if (w[r] > wmax) is_top[r] = 1;
+      else if (p < 0 || w[p] > wmax) roots.push_back(r);
+    }
+    S.border.clear();
+    for (size_t lv = 0; lv + 1 < S.dlev_ptr.size(); ++lv) {
+      std::vector<int32_t> tops;
+      for (int32_t q = S.dlev_ptr[lv]; q < S.dlev_ptr[lv + 1]; ++q)
+        if (is_top[S.dlev_sn[q]]) tops.push_back(S.dlev_sn[q]);
+      std::stable_sort(tops.begin(), tops.end(), [&](int32_t x, int32_t y) { return w[x] > w[y]; });
+      S.border.insert(S.border.end(), tops.begin(), tops.end());
+    }
+    S.ntop = (int32_t)S.border.size();
+    std::stable_sort(roots.begin(), roots.end(), [&](int32_t x, int32_t y) { return w[x] > w[y]; });
+    S.sub_ptr.assign(1, S.ntop);
+    std::vector<int32_t> stack;
+    for (int32_t rt : roots) {
+      stack.assign(1, rt);
+      while (!stack.empty()) {
+        const int32_t r = stack.back();
+        stack.pop_back();
+        S.border.push_back(r);
+        for (int32_t q = S.child_ptr[r + 1] - 1; q >= S.child_ptr[r]; --q) stack.push_back(S.child_list[q]);
+      }
+      S.sub_ptr.push_back((int32_t)S.border.size());
+    }
+    if ((int32_t)S.border.size() != ns) return "internal: backward task order incomplete";
+  }
   // within a depth level, the most work first (backward solve: one warp per supernode)
   for (size_t lv = 0; lv + 1 < S.dlev_ptr.size(); ++lv) {
     auto b = S.dlev_sn.begin() + S.dlev_ptr[lv], e = S.dlev_sn.begin() + S.dlev_ptr[lv + 1];

@@ -47,6 +47,10 @@ struct Symbolic {
   std::vector<int32_t> depth;            // per supernode, roots = 0
   std::vector<int32_t> dlev_ptr, dlev_sn;  // grouped by depth (backward solve)
   std::vector<int32_t> preorder;           // supernodes, parents before children, subtrees contiguous
+  // backward-solve task order: ntop top supernodes (level order, most work first), then subtrees
+  // (each contiguous in preorder, biggest first); sub_ptr offsets into border
+  std::vector<int32_t> border, sub_ptr;
+  int32_t ntop = 0;
 
   int64_t nnzE() const { return colptr.empty() ? 0 : colptr.back(); }
 };
