@@ -61,12 +61,27 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
 #pragma unroll
     for (int j = 0; j < kCh; ++j) acc[j] = (j < w && onpath) ? xrow(X, f + t0 + j, lane) : 0.0;
     const double* Lc = Lr + (size_t)t0 * c;  // Lc[i + j*c] = L[i, t0+j]
-#pragma unroll 2
-    for (int q = 0; q < u; ++q) {
-      const double xq = xrow(X, U[q], lane);
+    // U rows in blocks of 32: indices and L values loaded coalesced by the warp, broadcast by
+    // shuffles; 8 independent row loads in flight
+    for (int q0 = 0; q0 < u; q0 += 32) {
+      const int nq = min(32, u - q0);
+      const int myrow = lane < nq ? U[q0 + lane] : 0;
+      double lv[kCh];
 #pragma unroll
-      for (int j = 0; j < kCh; ++j)
-        if (j < w) acc[j] -= Lc[s + q + (size_t)j * c] * xq;
+      for (int j = 0; j < kCh; ++j) lv[j] = (j < w && lane < nq) ? Lc[s + q0 + lane + (size_t)j * c] : 0.0;
+      for (int k0 = 0; k0 < nq; k0 += 8) {
+        double xq[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int rr = __shfl_sync(0xffffffffu, myrow, k0 + k);
+          xq[k] = (k0 + k < nq) ? xrow(X, rr, lane) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#pragma unroll
+          for (int j = 0; j < kCh; ++j) acc[j] -= __shfl_sync(0xffffffffu, lv[j], k0 + k) * xq[k];
+        }
+      }
     }
     for (int tp = t1; tp < s; ++tp) {
       const double xq = xrow(X, f + tp, lane);
@@ -107,7 +122,7 @@ __device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c,
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ uint32_t inreach[];  // bitmap over supernodes
   const int P = blockIdx.x, fac = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
