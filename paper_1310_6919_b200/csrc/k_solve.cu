@@ -9,10 +9,9 @@
 // Per panel P (columns p0 = 32P .. p0+31, elimination order):
 //   forward  L z = E_P  over the union of the etree paths of the panel's columns (ascending
 //            supernodes, whole CTA per supernode; rows off the paths are exactly zero); z <- D^{-1} z;
-//   backward L^T x = z  over all supernodes, one warp per task, dataflow: the top of the tree one
-//            supernode per task in level order, then whole bottom subtrees per warp in preorder; a task
-//            starts when its parent is done (no write conflicts: a supernode writes only its rows S_r
-//            and reads ancestors' rows U_r).
+//   backward L^T x = z  the top of the tree (big supernodes) one supernode at a time by the whole CTA,
+//            then whole bottom subtrees, one warp each, in preorder (no write conflicts: a supernode
+//            writes only its rows S_r and reads its ancestors' rows U_r).
 // Both sweeps keep up to 16 columns of a supernode in registers, so every row x[U_q] is read once
 // per 16 columns (not once per column).
 // Output layout: panel-major, X[P][i][lane] (row i of the panel = 32 contiguous doubles).
@@ -101,6 +100,79 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
   }
 }
 
+// ---- CTA-cooperative pieces for big supernodes (all warps, CTA barriers) ----
+// backward, step 1: X[f+t] = y_t - sum_q L[s+q, t] x[U_q] for all t in S (columns over warps, 8 per pass)
+__device__ __forceinline__ void coop_bwd_gemv(const double* __restrict__ Lr, int c, int s, int f,
+                                              const int32_t* __restrict__ U, double* X, int lane, int wid,
+                                              int nw, bool onpath) {
+  const int u = c - s;
+  for (int tb = wid; tb < s; tb += 8 * nw) {  // columns tb, tb+nw, ..., tb+7nw
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = tb + j * nw;
+      acc[j] = (t < s && onpath) ? xrow(X, f + t, lane) : 0.0;
+    }
+    for (int q = 0; q < u; ++q) {
+      const double xq = xrow(X, U[q], lane);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int t = tb + j * nw;
+        if (t < s) acc[j] -= Lr[s + q + (size_t)t * c] * xq;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = tb + j * nw;
+      if (t < s) xrow(X, f + t, lane) = acc[j];
+    }
+  }
+}
+
+// backward, step 2: x[S] = L_SS^{-T} acc, blocked by 16 from the last block
+__device__ __forceinline__ void coop_bwd_tri(const double* __restrict__ Lr, int c, int s, int f, double* X,
+                                             int lane, int wid, int nw) {
+  for (int t1 = s; t1 > 0; t1 -= 16) {
+    const int t0 = t1 > 16 ? t1 - 16 : 0;
+    if (wid == 0) {
+      for (int t = t1 - 1; t >= t0; --t) {
+        double v = xrow(X, f + t, lane);
+        for (int tp = t + 1; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * xrow(X, f + tp, lane);
+        xrow(X, f + t, lane) = v;
+      }
+    }
+    __syncthreads();
+    for (int t = wid; t < t0; t += nw) {
+      double v = xrow(X, f + t, lane);
+      for (int tp = t0; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * xrow(X, f + tp, lane);
+      xrow(X, f + t, lane) = v;
+    }
+    __syncthreads();
+  }
+}
+
+// forward triangle z[S] = L_SS^{-1} z[S] (unit lower), blocked by 16 from the first block
+__device__ __forceinline__ void coop_fwd_tri(const double* __restrict__ Lr, int c, int s, int f, double* X,
+                                             int lane, int wid, int nw) {
+  for (int t0 = 0; t0 < s; t0 += 16) {
+    const int t1 = min(s, t0 + 16);
+    if (wid == 0) {
+      for (int t = t0 + 1; t < t1; ++t) {
+        double v = xrow(X, f + t, lane);
+        for (int tp = t0; tp < t; ++tp) v -= Lr[t + (size_t)tp * c] * xrow(X, f + tp, lane);
+        xrow(X, f + t, lane) = v;
+      }
+    }
+    __syncthreads();
+    for (int t = t1 + wid; t < s; t += nw) {
+      double v = xrow(X, f + t, lane);
+      for (int tp = t0; tp < t1; ++tp) v -= Lr[t + (size_t)tp * c] * xrow(X, f + tp, lane);
+      xrow(X, f + t, lane) = v;
+    }
+    __syncthreads();
+  }
+}
+
 // forward update of the U rows of one supernode by all warps: x[U] -= L_US z[S] (S rows final)
 template <int kCh>
 __device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c, int s, int f,
@@ -155,31 +227,26 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
     const double* Lr = Lp + a.panel_off[r];
-    if (wid == 0) {  // unit lower diagonal block, register chunks of kCh rows
-      for (int t0 = 0; t0 < s; t0 += kCh) {
-        const int w = min(kCh, s - t0);
-        double acc[kCh];
+    if (s > 16) {
+      coop_fwd_tri(Lr, c, s, f, X, lane, wid, NW);
+    } else {
+      if (wid == 0) {  // unit lower diagonal block in registers
+        double acc[16];
 #pragma unroll
-        for (int j = 0; j < kCh; ++j) acc[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
-        for (int tp = 0; tp < t0; ++tp) {
-          const double zt = xrow(X, f + tp, lane);
+        for (int j = 0; j < 16; ++j) acc[j] = j < s ? xrow(X, f + j, lane) : 0.0;
 #pragma unroll
-          for (int j = 0; j < kCh; ++j)
-            if (j < w) acc[j] -= Lr[(t0 + j) + (size_t)tp * c] * zt;
-        }
-#pragma unroll
-        for (int j = 0; j < kCh; ++j) {
-          if (j < w) {
+        for (int j = 0; j < 16; ++j) {
+          if (j < s) {
             const double zj = acc[j];
-            xrow(X, f + t0 + j, lane) = zj;
+            xrow(X, f + j, lane) = zj;
 #pragma unroll
-            for (int jj = j + 1; jj < kCh; ++jj)
-              if (jj < w) acc[jj] -= Lr[(t0 + jj) + (size_t)(t0 + j) * c] * zj;
+            for (int jj = j + 1; jj < 16; ++jj)
+              if (jj < s) acc[jj] -= Lr[jj + (size_t)j * c] * zj;
           }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
     if (u > 0) {
       const int32_t* U = rowind + a.colptr[f] + s;
       if (s <= 1) fwd_update<1>(Lr, c, s, f, U, X, lane, wid, NW);
@@ -193,38 +260,28 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   }
   __syncthreads();
 
-  // backward L^T x = z, dataflow: tasks are (a) single supernodes of the top of the tree, claimed
-  // in level order, each waiting for its parent's done flag, then (b) whole bottom subtrees, each
-  // processed by one warp in preorder (parents' rows are reused immediately).  Rows off the paths
-  // have z = 0.
-  uint32_t* done = inreach + nwords;
-  for (int i = tid; i < nwords; i += kSolveThreads) done[i] = 0;
-  int* ctr = reinterpret_cast<int*>(done + nwords);
+  // backward L^T x = z.  (1) the top of the tree (big supernodes near the roots) in level order,
+  // each supernode by the whole CTA; (2) the remaining subtrees, one warp per subtree in preorder,
+  // claimed from a shared counter (no waiting: their only outside dependencies are in the top).
+  // Rows off the paths have z = 0.
+  for (int it = 0; it < a.ntop; ++it) {
+    const int r = a.border[it];
+    const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
+    const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
+    const double* Lr = Lp + a.panel_off[r];
+    coop_bwd_gemv(Lr, c, s, f, rowind + a.colptr[f] + s, X, lane, wid, NW, onpath);
+    __syncthreads();
+    coop_bwd_tri(Lr, c, s, f, X, lane, wid, NW);
+  }
+  int* ctr = reinterpret_cast<int*>(inreach + nwords);
   if (tid == 0) *ctr = 0;
   __syncthreads();
-  const int ntask = a.ntop + a.nsub;
   for (;;) {
     int q = 0;
     if (lane == 0) q = atomicAdd(ctr, 1);
     q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= ntask) break;
-    int b, e;
-    if (q < a.ntop) {
-      b = q;
-      e = q + 1;
-    } else {
-      b = a.sub_ptr[q - a.ntop];
-      e = a.sub_ptr[q - a.ntop + 1];
-    }
-    {  // wait for the parent of the first node (top node or subtree root)
-      const int pr = a.sparent[a.border[b]];
-      if (pr >= 0) {
-        volatile uint32_t* dv = done;
-        while (((dv[pr >> 5] >> (pr & 31)) & 1u) == 0) __nanosleep(20);
-        __threadfence_block();
-      }
-    }
-    for (int it = b; it < e; ++it) {
+    if (q >= a.nsub) break;
+    for (int it = a.sub_ptr[q]; it < a.sub_ptr[q + 1]; ++it) {
       const int r = a.border[it];
       const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
       const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
@@ -235,12 +292,6 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
       else if (s <= 4) bwd_supernode<4>(Lr, c, s, f, U, X, lane, onpath);
       else if (s <= 8) bwd_supernode<8>(Lr, c, s, f, U, X, lane, onpath);
       else bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
-    }
-    if (q < a.ntop) {
-      __threadfence_block();
-      __syncwarp();
-      const int r = a.border[b];
-      if (lane == 0) atomicOr(&done[r >> 5], 1u << (r & 31));
     }
   }
 }
@@ -271,7 +322,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.D[1] = h->Dy;
   a.out[0] = h->Xh;
   a.out[1] = h->Yh;
-  size_t smem = sizeof(uint32_t) * (2 * ((h->S.nsuper + 31) / 32) + 1);
+  size_t smem = sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
   static bool attr = false;
   if (!attr && smem > 48 * 1024) {
     cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
