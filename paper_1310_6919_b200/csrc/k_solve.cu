@@ -100,76 +100,98 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
   }
 }
 
-// ---- CTA-cooperative pieces for big supernodes (all warps, CTA barriers) ----
-// backward, step 1: X[f+t] = y_t - sum_q L[s+q, t] x[U_q] for all t in S (columns over warps, 8 per pass)
-__device__ __forceinline__ void coop_bwd_gemv(const double* __restrict__ Lr, int c, int s, int f,
-                                              const int32_t* __restrict__ U, double* X, int lane, int wid,
-                                              int nw, bool onpath) {
-  const int u = c - s;
-  for (int tb = wid; tb < s; tb += 8 * nw) {  // columns tb, tb+nw, ..., tb+7nw
-    double acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int t = tb + j * nw;
-      acc[j] = (t < s && onpath) ? xrow(X, f + t, lane) : 0.0;
-    }
-    for (int q = 0; q < u; ++q) {
-      const double xq = xrow(X, U[q], lane);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int t = tb + j * nw;
-        if (t < s) acc[j] -= Lr[s + q + (size_t)t * c] * xq;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int t = tb + j * nw;
-      if (t < s) xrow(X, f + t, lane) = acc[j];
-    }
+// ---- CTA-cooperative pieces (all warps, CTA barriers), rows staged in shared memory ----
+constexpr int kStageRows = 384;  // rows of 256 B staged per CTA (96 KB)
+
+// stage rows S (zero if !s_valid) then U of a supernode into R[0..s+u) with cp.async
+__device__ __forceinline__ void stage_rows(double* R, const double* X, int f, int s, const int32_t* __restrict__ U,
+                                           int u, bool s_valid, int tid, int nt) {
+  for (int idx = tid; idx < (s + u) * 16; idx += nt) {
+    const int row = idx >> 4, ch = idx & 15;
+    const int src = row < s ? f + row : U[row - s];
+    const bool v = row < s ? s_valid : true;
+    cp_async16(R + row * kPanelW + ch * 2, X + (size_t)src * kPanelW + ch * 2, v);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
 }
 
-// backward, step 2: x[S] = L_SS^{-T} acc, blocked by 16 from the last block
-__device__ __forceinline__ void coop_bwd_tri(const double* __restrict__ Lr, int c, int s, int f, double* X,
-                                             int lane, int wid, int nw) {
+// backward for a staged supernode: R[t] = y_t - sum_q L[s+q,t] R[s+q]; then x[S] = L_SS^{-T} R[S]
+__device__ __forceinline__ void coop_bwd_staged(const double* __restrict__ Lr, int c, int s, double* R, int lane,
+                                                int wid, int nw) {
+  const int u = c - s;
+  for (int t = wid; t < s; t += nw) {
+    const double* Lt = Lr + s + (size_t)t * c;
+    double a0 = R[t * kPanelW + lane], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int q = 0;
+    for (; q + 3 < u; q += 4) {
+      a0 -= Lt[q] * R[(s + q) * kPanelW + lane];
+      a1 -= Lt[q + 1] * R[(s + q + 1) * kPanelW + lane];
+      a2 -= Lt[q + 2] * R[(s + q + 2) * kPanelW + lane];
+      a3 -= Lt[q + 3] * R[(s + q + 3) * kPanelW + lane];
+    }
+    for (; q < u; ++q) a0 -= Lt[q] * R[(s + q) * kPanelW + lane];
+    R[t * kPanelW + lane] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
   for (int t1 = s; t1 > 0; t1 -= 16) {
     const int t0 = t1 > 16 ? t1 - 16 : 0;
     if (wid == 0) {
       for (int t = t1 - 1; t >= t0; --t) {
-        double v = xrow(X, f + t, lane);
-        for (int tp = t + 1; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * xrow(X, f + tp, lane);
-        xrow(X, f + t, lane) = v;
+        double v = R[t * kPanelW + lane];
+        for (int tp = t + 1; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * R[tp * kPanelW + lane];
+        R[t * kPanelW + lane] = v;
       }
     }
     __syncthreads();
     for (int t = wid; t < t0; t += nw) {
-      double v = xrow(X, f + t, lane);
-      for (int tp = t0; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * xrow(X, f + tp, lane);
-      xrow(X, f + t, lane) = v;
+      double v = R[t * kPanelW + lane];
+      for (int tp = t0; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * R[tp * kPanelW + lane];
+      R[t * kPanelW + lane] = v;
     }
     __syncthreads();
   }
 }
 
-// forward triangle z[S] = L_SS^{-1} z[S] (unit lower), blocked by 16 from the first block
-__device__ __forceinline__ void coop_fwd_tri(const double* __restrict__ Lr, int c, int s, int f, double* X,
-                                             int lane, int wid, int nw) {
+// forward triangle on staged S rows: R[S] = L_SS^{-1} R[S] (unit lower), blocked by 16
+__device__ __forceinline__ void coop_fwd_tri_staged(const double* __restrict__ Lr, int c, int s, double* R, int lane,
+                                                    int wid, int nw) {
   for (int t0 = 0; t0 < s; t0 += 16) {
     const int t1 = min(s, t0 + 16);
     if (wid == 0) {
       for (int t = t0 + 1; t < t1; ++t) {
-        double v = xrow(X, f + t, lane);
-        for (int tp = t0; tp < t; ++tp) v -= Lr[t + (size_t)tp * c] * xrow(X, f + tp, lane);
-        xrow(X, f + t, lane) = v;
+        double v = R[t * kPanelW + lane];
+        for (int tp = t0; tp < t; ++tp) v -= Lr[t + (size_t)tp * c] * R[tp * kPanelW + lane];
+        R[t * kPanelW + lane] = v;
       }
     }
     __syncthreads();
     for (int t = t1 + wid; t < s; t += nw) {
-      double v = xrow(X, f + t, lane);
-      for (int tp = t0; tp < t1; ++tp) v -= Lr[t + (size_t)tp * c] * xrow(X, f + tp, lane);
-      xrow(X, f + t, lane) = v;
+      double v = R[t * kPanelW + lane];
+      for (int tp = t0; tp < t1; ++tp) v -= Lr[t + (size_t)tp * c] * R[tp * kPanelW + lane];
+      R[t * kPanelW + lane] = v;
     }
     __syncthreads();
+  }
+}
+
+// forward U update from staged S rows: x[U_q] -= sum_t L[s+q, t] R[t], 2 rows per warp in flight
+__device__ __forceinline__ void coop_fwd_update_staged(const double* __restrict__ Lr, int c, int s,
+                                                       const int32_t* __restrict__ U, const double* R, double* X,
+                                                       int lane, int wid, int nw) {
+  const int u = c - s;
+  for (int qq = wid; qq < u; qq += 2 * nw) {
+    const int q2 = qq + nw;
+    const int r1 = U[qq], r2 = q2 < u ? U[q2] : r1;
+    double x1 = xrow(X, r1, lane), x2 = q2 < u ? xrow(X, r2, lane) : 0.0;
+    for (int t = 0; t < s; ++t) {
+      const double z = R[t * kPanelW + lane];
+      x1 -= Lr[s + qq + (size_t)t * c] * z;
+      if (q2 < u) x2 -= Lr[s + q2 + (size_t)t * c] * z;
+    }
+    xrow(X, r1, lane) = x1;
+    if (q2 < u) xrow(X, r2, lane) = x2;
   }
 }
 
@@ -195,7 +217,9 @@ __device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c,
 }
 
 __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
-  extern __shared__ uint32_t inreach[];  // bitmap over supernodes
+  extern __shared__ __align__(16) double smem_solve[];
+  double* R = smem_solve;                                                               // staged rows
+  uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + kStageRows * kPanelW);  // bitmap
   const int P = blockIdx.x, fac = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSolveThreads / 32;
@@ -227,33 +251,46 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
     const double* Lr = Lp + a.panel_off[r];
-    if (s > 16) {
-      coop_fwd_tri(Lr, c, s, f, X, lane, wid, NW);
+    if (s > 16 && s <= kStageRows) {
+      // big supernode: S rows staged in shared memory, triangle and U update from there
+      stage_rows(R, X, f, s, nullptr, 0, true, tid, kSolveThreads);
+      coop_fwd_tri_staged(Lr, c, s, R, lane, wid, NW);
+      for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) = R[t * kPanelW + lane];
+      if (u > 0) coop_fwd_update_staged(Lr, c, s, rowind + a.colptr[f] + s, R, X, lane, wid, NW);
     } else {
-      if (wid == 0) {  // unit lower diagonal block in registers
-        double acc[16];
+      if (wid == 0) {  // unit lower diagonal block in registers, chunks of 16
+        for (int t0 = 0; t0 < s; t0 += 16) {
+          const int w = min(16, s - t0);
+          double acc[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = j < s ? xrow(X, f + j, lane) : 0.0;
+          for (int j = 0; j < 16; ++j) acc[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
+          for (int tp = 0; tp < t0; ++tp) {
+            const double zt = xrow(X, f + tp, lane);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j < s) {
-            const double zj = acc[j];
-            xrow(X, f + j, lane) = zj;
+            for (int j = 0; j < 16; ++j)
+              if (j < w) acc[j] -= Lr[(t0 + j) + (size_t)tp * c] * zt;
+          }
 #pragma unroll
-            for (int jj = j + 1; jj < 16; ++jj)
-              if (jj < s) acc[jj] -= Lr[jj + (size_t)j * c] * zj;
+          for (int j = 0; j < 16; ++j) {
+            if (j < w) {
+              const double zj = acc[j];
+              xrow(X, f + t0 + j, lane) = zj;
+#pragma unroll
+              for (int jj = j + 1; jj < 16; ++jj)
+                if (jj < w) acc[jj] -= Lr[(t0 + jj) + (size_t)(t0 + j) * c] * zj;
+            }
           }
         }
       }
       __syncthreads();
-    }
-    if (u > 0) {
-      const int32_t* U = rowind + a.colptr[f] + s;
-      if (s <= 1) fwd_update<1>(Lr, c, s, f, U, X, lane, wid, NW);
-      else if (s <= 2) fwd_update<2>(Lr, c, s, f, U, X, lane, wid, NW);
-      else if (s <= 4) fwd_update<4>(Lr, c, s, f, U, X, lane, wid, NW);
-      else if (s <= 8) fwd_update<8>(Lr, c, s, f, U, X, lane, wid, NW);
-      else fwd_update<16>(Lr, c, s, f, U, X, lane, wid, NW);
+      if (u > 0) {
+        const int32_t* U = rowind + a.colptr[f] + s;
+        if (s <= 1) fwd_update<1>(Lr, c, s, f, U, X, lane, wid, NW);
+        else if (s <= 2) fwd_update<2>(Lr, c, s, f, U, X, lane, wid, NW);
+        else if (s <= 4) fwd_update<4>(Lr, c, s, f, U, X, lane, wid, NW);
+        else if (s <= 8) fwd_update<8>(Lr, c, s, f, U, X, lane, wid, NW);
+        else fwd_update<16>(Lr, c, s, f, U, X, lane, wid, NW);
+      }
     }
     __syncthreads();
     for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) /= D[f + t];
@@ -269,9 +306,15 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
     const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
     const double* Lr = Lp + a.panel_off[r];
-    coop_bwd_gemv(Lr, c, s, f, rowind + a.colptr[f] + s, X, lane, wid, NW, onpath);
+    const int32_t* U = rowind + a.colptr[f] + s;
+    if (c <= kStageRows) {
+      stage_rows(R, X, f, s, U, c - s, onpath, tid, kSolveThreads);
+      coop_bwd_staged(Lr, c, s, R, lane, wid, NW);
+      for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) = R[t * kPanelW + lane];
+    } else if (wid == 0) {  // very large clique: one warp from global memory
+      bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
+    }
     __syncthreads();
-    coop_bwd_tri(Lr, c, s, f, X, lane, wid, NW);
   }
   int* ctr = reinterpret_cast<int*>(inreach + nwords);
   if (tid == 0) *ctr = 0;
@@ -322,10 +365,10 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.D[1] = h->Dy;
   a.out[0] = h->Xh;
   a.out[1] = h->Yh;
-  size_t smem = sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
+  size_t smem = sizeof(double) * kStageRows * kPanelW + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
   static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (!attr) {
+    cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     attr = true;
   }
   dim3 grid(h->d.npanels, 2);
