@@ -31,10 +31,10 @@ constexpr int kLdS = kTile + 4;  // smem row stride (doubles): conflict-free fra
 constexpr int kGemmThreads = 256;
 
 // ------------------------------------------------------------------ diagonal block
-constexpr int kDiagThreads = 512;
+constexpr int kDiagThreads = 256;
 constexpr int kLdD = kNB + 1;  // A[i + j*kLdD]
 
-__global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
+__global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
   extern __shared__ double sm[];
@@ -53,37 +53,69 @@ __global__ void __launch_bounds__(kDiagThreads) potrf_diag_kernel(double* B, int
     A[i + j * kLdD] = v;
   }
   __syncthreads();
-  const int row = tid & (kNB - 1), slice = tid >> 7;  // 4 slices of 8 columns
+  // 32-column panels.  (1) warp 0 factors the 32 x 32 diagonal sub-block in registers (lane = row,
+  // shuffles, rsqrt) and inverts it (lane = column, broadcast reads); (2) all threads form the panel
+  // rows below with that inverse; (3) register-tiled trailing update.
+  __shared__ double inv32[32][33];
+  __shared__ int fail_col;
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll 1
   for (int jb = 0; jb < kNB; jb += 32) {
-    // column by column inside the panel, one barrier per column: the update uses the unscaled
-    // column j (A[i,k] -= A[i,j] A[k,j] / d); the scaled column goes to P.
-    for (int j = jb; j < jb + 32; ++j) {
-      const double d = A[j + j * kLdD];
-      if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
-        if (tid == 0) report_error(err, k0 + j + 1);
-        return;
+    if (wid == 0) {
+      // factor the 32 x 32 block in place in shared memory: lane = row jb+lane
+      double* Ab = A + jb + jb * kLdD;  // Ab[i + k*kLdD]
+      int fail = -1;
+      double rdiag = 0.0;
+      for (int j = 0; j < 32; ++j) {
+        const double d = Ab[j + j * kLdD];
+        if (!(d > 0.0)) {  // uniform across the warp
+          fail = j;
+          break;
+        }
+        const double r = rsqrt(d);
+        const double l = Ab[lane + j * kLdD] * r;
+        if (lane == j) rdiag = r;
+        __syncwarp();
+        if (lane >= j) Ab[lane + j * kLdD] = l;
+        __syncwarp();
+        if (lane > j) {
+#pragma unroll 4
+          for (int k = j + 1; k <= lane; ++k) Ab[lane + k * kLdD] -= l * Ab[k + j * kLdD];
+        }
+        __syncwarp();
       }
-      const double inv_d = 1.0 / d;
-      const double aij = (row >= j) ? A[row + j * kLdD] : 0.0;
-      if (slice == 0 && row >= j) P[j - jb][row] = aij * rsqrt(d);
-      if (row > j) {
-        const double fi = aij * inv_d;
-        const int kbeg = jb + slice * 8;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int k = kbeg + q;
-          if (k > j && k <= row) A[row + k * kLdD] -= fi * A[k + j * kLdD];
+      if (lane == 0) fail_col = fail;
+      if (fail < 0) {
+        // inverse: lane = column c; x_i = (delta_ic - sum_{k<i} L[i][k] x_k) / L[i][i]
+        for (int i = 0; i < 32; ++i) {
+          double sacc = (i == lane) ? 1.0 : 0.0;
+          for (int k = lane; k < i; ++k) sacc -= Ab[i + k * kLdD] * inv32[k][lane];
+          inv32[i][lane] = (i >= lane) ? sacc * __shfl_sync(0xffffffffu, rdiag, i) : 0.0;
+          __syncwarp();
         }
       }
-      __syncthreads();
     }
-    for (int idx = tid; idx < 32 * kNB; idx += kDiagThreads) {
-      const int k = idx >> 7, i = idx & (kNB - 1);
-      if (i >= jb + k) A[i + (jb + k) * kLdD] = P[k][i];
+    __syncthreads();
+    if (fail_col >= 0) {
+      if (tid == 0) report_error(err, k0 + jb + fail_col + 1);
+      return;
     }
-    // trailing update of rows/cols >= jb+32 with the panel: 4 x 4 register tiles
     const int r0 = jb + 32, nr = kNB - r0;
     if (nr > 0) {
+      // panel rows below: L[i, jb+c] = sum_{k>=c} A[i, jb+k] Linv[c][k]... (L21 = A21 L11^{-T})
+      for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
+        const int i = r0 + (idx & 31) + (idx >> 10) * 32, c = (idx >> 5) & 31;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int k = 0; k <= 31; ++k) acc += A[i + (jb + k) * kLdD] * inv32[c][k];
+        P[c][i] = acc;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
+        const int c = idx / nr, i = r0 + idx % nr;
+        A[i + (jb + c) * kLdD] = P[c][i];
+      }
+      // trailing update of rows/cols >= r0 with the panel: 4 x 4 register tiles
       const int nb4 = nr / 4;
       const int ntile = nb4 * (nb4 + 1) / 2;
       for (int t = tid; t < ntile; t += kDiagThreads) {
