@@ -85,17 +85,22 @@ typedef struct {
  *   perm[n]     : elimination order, perm[new] = old; NULL => built-in exact minimum degree
  *                 (ties -> smallest original id).
  *   device      : CUDA device ordinal this handle runs on.
- *   nranks, rank, nccl_id : multi-GPU world (nranks == 1: rank 0, nccl_id NULL).
+ *   nranks, rank : multi-GPU world.  B is distributed 2D block-cyclically
+ *                 in kScmNB = 256 tiles over a Pr x Pc grid (Pr = largest divisor of nranks
+ *                 <= sqrt(nranks); rank = myrow * Pc + mycol; see sdpc_get_scm_layout).  Each
+ *                 rank builds exactly its own tiles of B (columns l with (l/256) mod Pc == mycol
+ *                 need the RHS x_p, y_q of A_l only, Eq. newSCM2: columns of B are
+ *                 independent); (a1)/(a2) are replicated.  The library holds no
+ *                 communicator: the caller moves tiles between ranks (torch.distributed / NCCL)
+ *                 around the tile entries below.
+ *   nccl_id     : reserved, must be NULL.
  * Host arrays are copied.  Errors: INVALID_ARG (sizes, out-of-range ids, row < col,
- * perm not a permutation), OOM, CUDA (no device / not sm_100), NCCL.
+ * perm not a permutation, rank outside [0, nranks)), OOM, CUDA (no device / not sm_100).
  */
 sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m,
                         const int64_t* a_ptr, const int32_t* a_row, const int32_t* a_col,
                         const double* a_val, const double* b, const int32_t* perm,
                         int32_t device, int32_t nranks, int32_t rank, const void* nccl_id);
-
-/* 128-byte ncclUniqueId for multi-GPU handles (rank 0 creates, the caller broadcasts). */
-sdpc_status sdpc_get_unique_id(void* id_out /* 128 bytes */);
 
 sdpc_status sdpc_get_structure(sdpc_handle h, sdpc_structure* out);
 sdpc_status sdpc_get_scm_layout(sdpc_handle h, sdpc_layout* out);
@@ -121,7 +126,8 @@ sdpc_status sdpc_get_xinv_factor(sdpc_handle h, double* L_E, double* D, void* st
  * The strict upper triangle of B is not referenced.
  *   y_E : DEVICE [nnzE] fp64, Y on E in E's CSC order.
  *   B   : DEVICE, m x m column-major with leading dimension ldb >= m (nranks == 1), or this
- *         rank's local 2D block-cyclic buffer (sdpc_get_scm_layout) when nranks > 1.
+ *         rank's local 2D block-cyclic array (mloc x nloc, ldb >= lld; sdpc_get_scm_layout)
+ *         when nranks > 1: only the rank's own tiles are written, at local addresses.
  * Requires a successful sdpc_factor_xinv on this handle (else STATE).
  */
 sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t ldb, void* stream);
@@ -144,6 +150,37 @@ sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t
  * nranks > 1: B is the local 2D block-cyclic buffer; the factorization is collective.
  */
 sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream);
+
+/*
+ * Tile entries of the distributed (nranks > 1) SCM Cholesky, a 2D block-cyclic right-looking
+ * blocked Cholesky (P:711-713 type (i), P:1012 SDPARA-C's distributed variant).
+ * Per step k (tile column k of size kb <= 256, global rows from k1 = 256 k):
+ *   owner of tile (k, k):  sdpc_potrf_tile   (factor the tile, 128-block inverses out)
+ *   process column k:      sdpc_trsm_panel   (its panel tiles <- A L_kk^{-T})
+ *   every rank:            sdpc_update_tiles (its trailing tiles -= panel panel^T)
+ * with the caller broadcasting the factored tile down the process column and gathering the panel
+ * to every rank between the calls.  All three are ASYNCHRONOUS: enqueued on `stream`, they return
+ * without synchronising (unlike the rest of this ABI).  Matrices are column-major DEVICE arrays.
+ *
+ * sdpc_potrf_tile: A (n x n, lda >= n, n <= 256) <- its lower Cholesky factor in place (upper
+ *   part untouched); inv (DEVICE, 2 x 128 x 128, column-major) <- inverses of the factor's two
+ *   128-diagonal blocks (input of sdpc_trsm_panel); info_dev (DEVICE int32) <- 0x7f7f7f7f if PD,
+ *   else the 1-based local column of the first non-positive pivot (LAPACK rule).
+ */
+sdpc_status sdpc_potrf_tile(sdpc_handle h, double* A, int32_t n, int64_t lda, double* inv,
+                            int32_t* info_dev, void* stream);
+
+/* sdpc_trsm_panel: A (rows x kb, lda >= rows) <- A L^{-T}, L = the kb x kb factored tile
+ * (ldl >= kb) and inv its block inverses from sdpc_potrf_tile.  Skipped if this handle's last
+ * sdpc_potrf_tile failed. */
+sdpc_status sdpc_trsm_panel(sdpc_handle h, double* A, int64_t rows, int64_t lda, const double* L,
+                            int64_t ldl, const double* inv, int32_t kb, void* stream);
+
+/* sdpc_update_tiles: for every local tile (I, J) of this rank with I >= J and 256 J >= k1:
+ * C_IJ -= P_I P_J^T (lower part only when I == J).  C = local array (mloc x nloc, ldc >= mloc);
+ * P = the gathered panel: row r is global row k1 + r (r < m - k1), K columns, ldp >= m - k1. */
+sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const double* P, int64_t ldp,
+                              int64_t k1, int32_t K, void* stream);
 
 /*
  * sdpc_iteration_host - the whole hot path from HOST buffers (what a host-side PDIPM driver

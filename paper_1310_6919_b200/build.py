@@ -33,11 +33,24 @@ def _compile(src: str, objdir: str, verbose: bool) -> str:
     return obj
 
 
+def source_hash() -> str:
+    """sha256 over every source, the header and this script (content, not mtimes: a snapshot copied
+    to another machine keeps its prebuilt library when nothing changed)."""
+    import hashlib
+    hsh = hashlib.sha256()
+    files = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh", ".cpp", ".hpp"))]
+    for f in files + [os.path.join(ROOT, "include", "sdpc.h"), os.path.abspath(__file__)]:
+        hsh.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            hsh.update(fh.read())
+    return hsh.hexdigest()
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = sources()
-    newest = max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC))
-    newest = max(newest, os.path.getmtime(os.path.join(ROOT, "include", "sdpc.h")), os.path.getmtime(__file__))
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
+    stamp = OUT + ".srchash"
+    want = source_hash()
+    if not force and os.path.exists(OUT) and os.path.exists(stamp) and open(stamp).read().strip() == want:
         return OUT
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
@@ -49,6 +62,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, OUT)
+    with open(stamp, "w") as fh:
+        fh.write(want + "\n")
     return OUT
 
 

@@ -119,11 +119,6 @@ int64_t sdpc_launch_count(sdpc_handle h) { return h ? h->launches : 0; }
 
 const char* sdpc_last_error_message(sdpc_handle h) { return h ? h->err.c_str() : ""; }
 
-sdpc_status sdpc_get_unique_id(void* id_out) {
-  (void)id_out;
-  return SDPC_ERR_NCCL;  // multi-GPU transport not built in this library version
-}
-
 sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a_ptr, const int32_t* a_row,
                         const int32_t* a_col, const double* a_val, const double* b, const int32_t* perm,
                         int32_t device, int32_t nranks, int32_t rank, const void* nccl_id) {
@@ -138,7 +133,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     if (!std::isfinite(b[k])) return SDPC_ERR_INVALID_ARG;
   for (int64_t e = 0; e < a_ptr[m + 1]; ++e)
     if (!std::isfinite(a_val[e])) return SDPC_ERR_INVALID_ARG;
-  if (nranks != 1 || rank != 0 || nccl_id != nullptr) return SDPC_ERR_INVALID_ARG;  // multi-GPU: not in this build
+  if (nranks < 1 || rank < 0 || rank >= nranks || nccl_id != nullptr) return SDPC_ERR_INVALID_ARG;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SDPC_ERR_CUDA;
@@ -149,6 +144,24 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   sdpc_ctx* h = new (std::nothrow) sdpc_ctx();
   if (!h) return SDPC_ERR_OOM;
   h->device = device;
+  h->nranks = nranks;
+  h->rank = rank;
+  // process grid Pr x Pc = nranks with Pr the largest divisor <= sqrt(nranks) (1x2, 2x2, 2x4, ...)
+  int Pr = 1;
+  for (int d0 = 1; (int64_t)d0 * d0 <= nranks; ++d0)
+    if (nranks % d0 == 0) Pr = d0;
+  h->grid.Pr = Pr;
+  h->grid.Pc = nranks / Pr;
+  h->grid.pr = rank / h->grid.Pc;
+  h->grid.pc = rank % h->grid.Pc;
+  auto numroc = [](int64_t m0, int64_t p, int64_t P) {  // ScaLAPACK numroc with tile kScmNB
+    const int64_t nt = (m0 + kScmNB - 1) / kScmNB;
+    int64_t cnt = 0;
+    for (int64_t t = p; t < nt; t += P) cnt += std::min<int64_t>(kScmNB, m0 - t * kScmNB);
+    return cnt;
+  };
+  h->mloc = numroc(m, h->grid.pr, h->grid.Pr);
+  h->nloc = numroc(m, h->grid.pc, h->grid.Pc);
   Symbolic& S = h->S;
   std::string msg = analyse(S, n, m, a_ptr, a_row, a_col, perm);
   if (!msg.empty()) {
@@ -185,22 +198,6 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     std::vector<int32_t> mem(S.hlev_sn.begin() + S.hlev_ptr[lv], S.hlev_sn.begin() + S.hlev_ptr[lv + 1]);
     std::stable_sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
     if (build_classes(h->a2lev[lv], mem, b2, ws_off, pb) != cudaSuccess) return fail(SDPC_ERR_OOM);
-  }
-
-  // ---- RHS panels: union of the etree paths of each panel's columns (supernode granularity)
-  const int32_t npanels = (n + kPanelW - 1) / kPanelW;
-  std::vector<int32_t> reach_ptr(npanels + 1, 0), reach_sn, stamp(ns, -1), tmp;
-  for (int32_t P = 0; P < npanels; ++P) {
-    tmp.clear();
-    for (int32_t p = P * kPanelW; p < std::min(n, (P + 1) * kPanelW); ++p) {
-      for (int32_t r = S.sn_of_col[p]; r >= 0 && stamp[r] != P; r = S.sparent[r]) {
-        stamp[r] = P;
-        tmp.push_back(r);
-      }
-    }
-    std::sort(tmp.begin(), tmp.end());
-    reach_sn.insert(reach_sn.end(), tmp.begin(), tmp.end());
-    reach_ptr[P + 1] = (int32_t)reach_sn.size();
   }
 
   // ---- constraints in elimination ids, symmetric expansion, duplicates summed
@@ -252,6 +249,42 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     }
   }
 
+  // ---- RHS slots: every vertex p that is a column of some A_l with l a column of B on this rank
+  // (Eq. newSCM2 needs x_p, v_p only for the nonzero columns p of A_l), ascending
+  // elimination ids so that a 32-slot panel shares most of its etree paths
+  std::vector<int32_t> rhs, slot_of(n, -1);
+  {
+    std::vector<uint8_t> need(n, 0);
+    for (int32_t l = 0; l < m; ++l) {
+      if (!h->grid.own_col(l)) continue;
+      for (int64_t e = cptr[l]; e < cptr[l + 1]; ++e) need[ci[e]] = 1;
+    }
+    for (int32_t v = 0; v < n; ++v)
+      if (need[v]) {
+        slot_of[v] = (int32_t)rhs.size();
+        rhs.push_back(v);
+      }
+  }
+  const int32_t nrhs = (int32_t)rhs.size();
+  const int32_t npanels = (nrhs + kPanelW - 1) / kPanelW;
+  rhs.resize((size_t)npanels * kPanelW, -1);
+  // per RHS panel: union of the etree paths of its vertices (supernode granularity)
+  std::vector<int32_t> reach_ptr(npanels + 1, 0), reach_sn, stamp(ns, -1), tmp;
+  for (int32_t P = 0; P < npanels; ++P) {
+    tmp.clear();
+    for (int32_t t = 0; t < kPanelW; ++t) {
+      const int32_t p = rhs[(size_t)P * kPanelW + t];
+      if (p < 0) continue;
+      for (int32_t r = S.sn_of_col[p]; r >= 0 && stamp[r] != P; r = S.sparent[r]) {
+        stamp[r] = P;
+        tmp.push_back(r);
+      }
+    }
+    std::sort(tmp.begin(), tmp.end());
+    reach_sn.insert(reach_sn.end(), tmp.begin(), tmp.end());
+    reach_ptr[P + 1] = (int32_t)reach_sn.size();
+  }
+
   // ---- upload
   DevSym& d = h->d;
   d.n = n;
@@ -259,6 +292,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   d.nsuper = ns;
   d.nnzE = S.nnzE();
   d.npanels = npanels;
+  d.nrhs = nrhs;
   cudaError_t e = cudaSuccess;
 #define UP(dst, v)                                    \
   if ((e = upload(&(dst), (v))) != cudaSuccess) { \
@@ -290,6 +324,9 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(d.iperm, S.iperm);
   UP(d.reach_ptr, reach_ptr);
   UP(d.reach_sn, reach_sn);
+  UP(d.rhs, rhs);
+  UP(d.slot_of, slot_of);
+  h->slot_of_host = slot_of;
   UP(h->d_ws_off, ws_off);
   DevCons& cs = h->cons;
   cs.maxcut = maxcut;
@@ -331,7 +368,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   DevSym& d = h->d;
   void* ptrs[] = {d.colptr, d.rowind, d.super_ptr, d.snc, d.sns, d.sparent, d.panel_off, d.e2p, d.umap_off,
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
-                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, h->d_ws_off,
+                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, h->d_ws_off,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
                   h->d_err, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
@@ -368,11 +405,14 @@ sdpc_status sdpc_get_structure(sdpc_handle h, sdpc_structure* out) {
 
 sdpc_status sdpc_get_scm_layout(sdpc_handle h, sdpc_layout* out) {
   if (!h || !out) return SDPC_ERR_INVALID_ARG;
-  out->nb = 128;
-  out->Pr = out->Pc = 1;
-  out->myrow = out->mycol = 0;
-  out->mloc = out->nloc = h->S.m;
-  out->lld = h->S.m;
+  out->nb = kScmNB;
+  out->Pr = h->grid.Pr;
+  out->Pc = h->grid.Pc;
+  out->myrow = h->grid.pr;
+  out->mycol = h->grid.pc;
+  out->mloc = h->mloc;
+  out->nloc = h->nloc;
+  out->lld = std::max<int64_t>(1, h->mloc);
   return SDPC_OK;
 }
 
@@ -435,12 +475,12 @@ sdpc_status sdpc_get_y_factor(sdpc_handle h, double* LY_E, double* DY, void* str
 }
 
 sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t ldb, void* stream) {
-  if (!h || !y_E || !B || ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
+  if (!h || !y_E || !B || ldb < std::max<int64_t>(1, h->mloc)) return SDPC_ERR_INVALID_ARG;
   if (!h->have_x) return SDPC_ERR_STATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   h->have_y = false;
-  const size_t dense = (size_t)h->d.npanels * h->S.n * kPanelW;
+  const size_t dense = std::max<size_t>(1, (size_t)h->d.npanels * h->S.n * kPanelW);
   if (!h->Xh) {
     CK(dalloc(&h->Xh, dense));
     CK(dalloc(&h->Yh, dense));
@@ -481,6 +521,7 @@ sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t
   for (int32_t c = 0; c < ncols; ++c) {
     if (cols[c] < 0 || cols[c] >= h->S.n) return SDPC_ERR_INVALID_ARG;
     cn[c] = h->S.iperm[cols[c]];
+    if (h->slot_of_host[cn[c]] < 0) return SDPC_ERR_INVALID_ARG;  // column not computed on this rank
   }
   int32_t* dc = nullptr;
   CK(upload(&dc, cn));
@@ -494,13 +535,14 @@ sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t
 
 sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream) {
   if (!h || !B || !info || ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
+  if (h->nranks != 1) return SDPC_ERR_STATE;  // distributed: sdpc_potrf_tile / trsm_panel / update_tiles
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(h->d_err, 0x7f, sizeof(int32_t), st));
   if (h->timing) CK(cudaEventRecord(h->ev[6], st));
   double fl = 0;
   int nu = 0;
-  h->launches += potrf_lower(h, B, h->S.m, ldb, h->d_err, st, &fl, &nu);
+  h->launches += potrf_lower(h, B, h->S.m, ldb, h->d_err, st, &fl, &nu, h->potrf_ws);
   if (h->timing) CK(cudaEventRecord(h->ev[7], st));
   int32_t v;
   sdpc_status s = check_err(h, st, &v);
@@ -525,6 +567,7 @@ sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* in
 sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const double* y_E, double* rdiag,
                                 int32_t* info, void* stream) {
   if (!h || !xbar_E || !y_E || !info) return SDPC_ERR_INVALID_ARG;
+  if (h->nranks != 1) return SDPC_ERR_STATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nnz = h->S.nnzE(), m = h->S.m;
@@ -553,6 +596,43 @@ sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const doubl
     std::memcpy(rdiag, h->pinned_out, sizeof(double) * m);
   }
   return s;
+}
+
+sdpc_status sdpc_potrf_tile(sdpc_handle h, double* A, int32_t n, int64_t lda, double* inv, int32_t* info_dev,
+                            void* stream) {
+  if (!h || !A || !inv || !info_dev || n < 1 || n > kScmNB || lda < n) return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(h->d_err, 0x7f, sizeof(int32_t), st));
+  const bool tim = h->timing;
+  h->timing = false;
+  h->launches += potrf_lower(h, A, n, lda, h->d_err, st, nullptr, nullptr, inv);
+  h->timing = tim;
+  CK(cudaMemcpyAsync(info_dev, h->d_err, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_trsm_panel(sdpc_handle h, double* A, int64_t rows, int64_t lda, const double* L, int64_t ldl,
+                            const double* inv, int32_t kb, void* stream) {
+  if (!h || rows < 0 || kb < 1 || kb > kScmNB || (rows > 0 && (!A || lda < rows)) || !L || ldl < kb || !inv)
+    return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  h->launches += trsm_panel(A, rows, lda, L, ldl, inv, kb, h->d_err, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1,
+                              int32_t K, void* stream) {
+  if (!h || k1 < 0 || K < 1 || K > kScmNB || k1 % kScmNB != 0) return SDPC_ERR_INVALID_ARG;
+  if (h->mloc > 0 && h->nloc > 0 && k1 < h->S.m && (!C || !P || ldc < h->mloc || ldp < h->S.m - k1))
+    return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  h->launches += update_tiles(C, ldc, P, ldp, k1, K, h->grid, h->S.m, h->mloc, h->nloc, h->d_err,
+                              (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return SDPC_OK;
 }
 
 sdpc_status sdpc_fp64_peak(int32_t device, double ms, double* dmma_tflops, double* dfma_tflops) {

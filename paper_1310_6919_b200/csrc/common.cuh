@@ -8,6 +8,22 @@ namespace sdpc {
 
 constexpr int kWarp = 32;
 constexpr int kPanelW = 32;  // RHS panel width of the multi-RHS solves: lane <-> RHS column
+constexpr int kScmNB = 256;  // tile size of the 2D block-cyclic distribution of B
+
+// 2D block-cyclic ownership of B (ScaLAPACK convention, rank = myrow * Pc + mycol): tile (I, J) of
+// size kScmNB lives on process (I mod Pr, J mod Pc) at local tile (I / Pr, J / Pc).  Pr = Pc = 1
+// reduces to the plain column-major B.
+struct Grid {
+  int Pr = 1, Pc = 1, pr = 0, pc = 0;
+  __host__ __device__ __forceinline__ bool own_row(int k) const { return (k / kScmNB) % Pr == pr; }
+  __host__ __device__ __forceinline__ bool own_col(int l) const { return (l / kScmNB) % Pc == pc; }
+  __host__ __device__ __forceinline__ int64_t lrow(int k) const {
+    return Pr == 1 ? k : (int64_t)(k / kScmNB / Pr) * kScmNB + k % kScmNB;
+  }
+  __host__ __device__ __forceinline__ int64_t lcol(int l) const {
+    return Pc == 1 ? l : (int64_t)(l / kScmNB / Pc) * kScmNB + l % kScmNB;
+  }
+};
 
 // Device error flag protocol: kernels atomicMin the failing index into *err
 // (initialised to kNoError by a byte memset).  Host reads it after the phase.

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "common.cuh"
 #include "symbolic.hpp"
 
 namespace sdpc {
@@ -40,6 +41,12 @@ struct DevSym {
   int32_t* reach_ptr = nullptr;  // per RHS panel: supernodes on the union of etree paths
   int32_t* reach_sn = nullptr;
   int32_t npanels = 0;
+  // RHS slots: the solves compute X-hat e_v and Y^{-1} e_v for v = rhs[s] (elimination id, -1 =
+  // padding), s = 32 P + lane; slot_of[v] = s or -1.  rhs = every vertex that is a column p of some
+  // A_l with l a column of B held by this rank (all touched vertices when nranks == 1).
+  int32_t* rhs = nullptr;
+  int32_t* slot_of = nullptr;
+  int32_t nrhs = 0;
 };
 
 // Size classes of the batched per-clique kernels ((a1) and (a2)).
@@ -72,6 +79,9 @@ struct DevCons {
 struct sdpc_ctx {
   int device = 0;
   int nranks = 1, rank = 0;
+  sdpc::Grid grid;                 // 2D block-cyclic process grid of B
+  std::vector<int32_t> slot_of_host;  // host copy of DevSym::slot_of
+  int64_t mloc = 0, nloc = 0;      // local rows / columns of B on this rank
   sdpc::Symbolic S;
   sdpc::DevSym d;
   sdpc::DevCons cons;
@@ -117,7 +127,12 @@ int launch_gather_columns(sdpc_ctx* h, const int32_t* d_cols_new, int32_t ncols,
 // Dense FP64 Cholesky of the lower triangle of B (m x m, ld).  Returns launches; info via d_err
 // (1-based failing column, kNoError if ok).  If upd_times, records an event pair per trailing update.
 int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st, double* flops_upd,
-                int* n_upd);
+                int* n_upd, double* linv_ws);
+// Distributed-Cholesky tile kernels; see sdpc.h.
+int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t ldl, const double* inv, int kb,
+               const int32_t* d_err, cudaStream_t st);
+int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1, int K, const Grid& g, int64_t m,
+                 int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st);
 int launch_diag_copy(double* B, int64_t m, int64_t ld, double* out, cudaStream_t st);
 cudaError_t fp64_peak(int device, double ms, double* dmma, double* dfma);
 }  // namespace sdpc

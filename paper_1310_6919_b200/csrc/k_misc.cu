@@ -20,12 +20,14 @@ int launch_panels_to_E(sdpc_ctx* h, const double* panels, double* E, cudaStream_
   return 1;
 }
 
-// out[o + c*n] = M_orig[o, col_c] for original row o; M is panel-major in elimination order.
+// out[o + c*n] = M_orig[o, col_c] for original row o; M is panel-major by RHS slot, rows in
+// elimination order.  Every requested column has a slot (checked on the host).
 __global__ void gather_columns_kernel(int n, int ncols, const int32_t* __restrict__ cols_new,
-                                      const int32_t* __restrict__ iperm, const double* __restrict__ Xh,
-                                      const double* __restrict__ Yh, double* Xo, double* Yo) {
+                                      const int32_t* __restrict__ slot_of, const int32_t* __restrict__ iperm,
+                                      const double* __restrict__ Xh, const double* __restrict__ Yh, double* Xo,
+                                      double* Yo) {
   const int c = blockIdx.y;
-  const int j = cols_new[c];
+  const int j = slot_of[cols_new[c]];
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
     const int i = iperm[o];
     const size_t idx = ((size_t)(j >> 5) * n + i) * kPanelW + (j & 31);
@@ -37,7 +39,7 @@ __global__ void gather_columns_kernel(int n, int ncols, const int32_t* __restric
 int launch_gather_columns(sdpc_ctx* h, const int32_t* d_cols_new, int32_t ncols, double* Xo, double* Yo,
                           cudaStream_t st) {
   dim3 grid((h->S.n + 255) / 256, ncols);
-  gather_columns_kernel<<<grid, 256, 0, st>>>(h->S.n, ncols, d_cols_new, h->d.iperm, h->Xh, h->Yh, Xo, Yo);
+  gather_columns_kernel<<<grid, 256, 0, st>>>(h->S.n, ncols, d_cols_new, h->d.slot_of, h->d.iperm, h->Xh, h->Yh, Xo, Yo);
   return 1;
 }
 

@@ -204,7 +204,11 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
   }
 }
 
-// ------------------------------------------------------------------ tensor-core GEMM (C op= A B^T)
+// ------------------------------------------------------------------ tensor-core GEMM
+// C op= A B^T on 128 x 128 tiles.  TRSM: C = A B^T (acc from zero; B = explicit L11^{-1}).
+// Updates (UPD*, RECT, DIST): the accumulators start as C (loaded straight into registers, so the HBM
+// read of C overlaps the operand pipeline instead of serialising behind the main loop) and the A
+// fragments are negated, so acc = C - A B^T; the epilogue only stores.
 struct GemmArgs {
   const double* A;  // element (i, kk) at A[i + kk*lda], i relative to the tile-row base
   int64_t lda;
@@ -212,13 +216,22 @@ struct GemmArgs {
   int64_t ldbm;
   double* C;  // element (i, j) at C[i + j*ldc]
   int64_t ldc;
-  int rows;   // valid rows of A (and of B for SYRK) from base 0
-  int cols;   // valid rows of B (TRSM: kb)
+  int rows;  // valid rows of A and C (UPD: also of B, the block is square)
+  int cols;  // TRSM / RECT: valid rows of B = columns of C
   int K;
+  int c0, c1;  // UPD: tile columns [c0, c1) (kModeUpdCols) or [c0, T) (kModeUpdTri)
+  // DIST: C is this rank's local 2D block-cyclic array (Grid), A = B = the gathered panel whose row 0
+  // is global row k1; local 128-row/column sub-tiles (blockIdx.x, blockIdx.y)
+  Grid g;
+  int64_t k1, m;
   const int32_t* err;
 };
 
-enum { kModeTrsm = 0, kModeSyrkAll = 1, kModeSyrkCol = 2, kModeSyrkRest = 3 };
+enum { kModeTrsm = 0, kModeUpdCols = 1, kModeUpdTri = 2, kModeRect = 3, kModeDist = 4 };
+
+__device__ __forceinline__ double neg(double x) {  // sign flip on the integer pipe
+  return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
+}
 
 template <int MODE, bool AL16>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
@@ -226,29 +239,59 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
   extern __shared__ double sm[];
   double* As = sm;                         // [kStages][kBK][kLdS]
   double* Bs = sm + kStages * kBK * kLdS;  // [kStages][kBK][kLdS]
-  int bi, bj;
-  if (MODE == kModeSyrkAll || MODE == kModeSyrkRest) {
-    const int t = blockIdx.x;
-    bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while (bi * (bi + 1) / 2 > t) --bi;
-    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-    bj = t - bi * (bi + 1) / 2;
-    if (MODE == kModeSyrkRest) {
-      ++bi;
-      ++bj;
-    }
+  constexpr bool UPD = MODE != kModeTrsm;
+  // tile -> operand bases, valid extents, and whether the tile straddles the diagonal (mask j > i)
+  const double* Ab;
+  const double* Bb;
+  double* Cb;
+  int na, nbv;
+  bool mask;
+  if (MODE == kModeTrsm || MODE == kModeRect) {
+    const int bi = blockIdx.x, bj = blockIdx.y;
+    Ab = g.A + (size_t)bi * kTile;
+    Bb = g.Bm + (size_t)bj * kTile;
+    Cb = g.C + (size_t)bi * kTile + (size_t)bj * kTile * g.ldc;
+    na = g.rows - bi * kTile;
+    nbv = g.cols - bj * kTile;
+    mask = false;
+  } else if (MODE == kModeDist) {
+    const int64_t la = (int64_t)blockIdx.x * kTile, lb = (int64_t)blockIdx.y * kTile;
+    const int64_t gi = ((la / kScmNB) * g.g.Pr + g.g.pr) * kScmNB + la % kScmNB;
+    const int64_t gj = ((lb / kScmNB) * g.g.Pc + g.g.pc) * kScmNB + lb % kScmNB;
+    if (gj < g.k1 || gi < gj || gi >= g.m) return;
+    Ab = g.A + (gi - g.k1);
+    Bb = g.A + (gj - g.k1);
+    Cb = g.C + la + lb * g.ldc;
+    na = (int)(g.m - gi < kTile ? g.m - gi : kTile);
+    nbv = (int)(g.m - gj < kTile ? g.m - gj : kTile);
+    mask = gi == gj;
   } else {
-    bi = blockIdx.x;
-    bj = 0;
+    const int T = (g.rows + kTile - 1) / kTile;
+    int t = blockIdx.x, bi, bj;
+    if (MODE == kModeUpdCols) {  // column-major over the few columns [c0, c1)
+      bj = g.c0;
+      while (t >= T - bj) {
+        t -= T - bj;
+        ++bj;
+      }
+      bi = bj + t;
+    } else {  // row-major over the lower triangle of tile columns [c0, T)
+      int r = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while (r * (r + 1) / 2 > t) --r;
+      while ((r + 1) * (r + 2) / 2 <= t) ++r;
+      bi = g.c0 + r;
+      bj = g.c0 + t - r * (r + 1) / 2;
+    }
+    Ab = g.A + (size_t)bi * kTile;
+    Bb = g.Bm + (size_t)bj * kTile;
+    Cb = g.C + (size_t)bi * kTile + (size_t)bj * kTile * g.ldc;
+    na = g.rows - bi * kTile;
+    nbv = g.rows - bj * kTile;
+    mask = bi == bj;
   }
-  constexpr bool SYRK = MODE != kModeTrsm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int wm = wid >> 2, wn = wid & 3;  // 2 x 4 warps, warp tile 64 x 32
   const int g8 = lane >> 2, t4 = lane & 3;
-  const int rowA0 = bi * kTile, rowB0 = bj * kTile;
-  const int rowsB = SYRK ? g.rows : g.cols;
-  const double* Ab = g.A + rowA0;
-  const double* Bb = g.Bm + rowB0;
 
   auto load_stage = [&](int stage, int k0) {
     double* as = As + stage * kBK * kLdS;
@@ -259,10 +302,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
         const int cid = tid + q * kGemmThreads;
         const int kk = cid / (kTile / 2), rp = (cid % (kTile / 2)) * 2;
         const bool kv = (k0 + kk) < g.K;
-        const bool va = kv && (rowA0 + rp) < g.rows;
+        const bool va = kv && rp < na;
         cp_async16(as + kk * kLdS + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
-        const bool vb = kv && (rowB0 + rp) < rowsB;
-        cp_async16(bs + kk * kLdS + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.Bm, vb);
+        const bool vb = kv && rp < nbv;
+        cp_async16(bs + kk * kLdS + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
       }
     } else {
 #pragma unroll
@@ -270,19 +313,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
         const int cid = tid + q * kGemmThreads;
         const int kk = cid / kTile, rp = cid % kTile;
         const bool kv = (k0 + kk) < g.K;
-        const bool va = kv && (rowA0 + rp) < g.rows;
+        const bool va = kv && rp < na;
         cp_async8(as + kk * kLdS + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
-        const bool vb = kv && (rowB0 + rp) < rowsB;
-        cp_async8(bs + kk * kLdS + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.Bm, vb);
+        const bool vb = kv && rp < nbv;
+        cp_async8(bs + kk * kLdS + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
       }
     }
   };
-
-  double acc[8][4][2];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   const int nk = (g.K + kBK - 1) / kBK;
 #pragma unroll
@@ -290,6 +327,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
     if (s < nk) load_stage(s, s * kBK);
     cp_async_commit();
   }
+
+  // accumulators: C (updates; lower part only of a diagonal tile) or zero (TRSM)
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int i = wm * 64 + a * 8 + g8;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = wn * 32 + b * 8 + 2 * t4 + e;
+        acc[a][b][e] = (UPD && i < na && j < nbv && (!mask || j <= i)) ? Cb[i + (size_t)j * g.ldc] : 0.0;
+      }
+  }
+
   for (int kc = 0; kc < nk; ++kc) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
@@ -302,7 +354,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
     for (int k4 = 0; k4 < kBK / 4; ++k4) {
       double af[8], bf[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) af[a] = as[(k4 * 4 + t4) * kLdS + wm * 64 + a * 8 + g8];
+      for (int a = 0; a < 8; ++a) {
+        const double v = as[(k4 * 4 + t4) * kLdS + wm * 64 + a * 8 + g8];
+        af[a] = UPD ? neg(v) : v;
+      }
 #pragma unroll
       for (int b = 0; b < 4; ++b) bf[b] = bs[(k4 * 4 + t4) * kLdS + wn * 32 + b * 8 + g8];
 #pragma unroll
@@ -313,48 +368,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // epilogue.  SYRK: C -= acc with all loads of a half-tile issued before any store (the
-  // compiler cannot reorder them itself because C's loads and stores may alias).
-  if (SYRK) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double cold[4][4][2];
+  for (int a = 0; a < 8; ++a) {
+    const int i = wm * 64 + a * 8 + g8;
+    if (i >= na) continue;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = rowA0 + wm * 64 + (h * 4 + a) * 8 + g8;
+    for (int b = 0; b < 4; ++b)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
-            cold[a][b][e] = (i < g.rows && j < g.rows && i >= j) ? g.C[i + (size_t)j * g.ldc] : 0.0;
-          }
+      for (int e = 0; e < 2; ++e) {
+        const int j = wn * 32 + b * 8 + 2 * t4 + e;
+        if (j < nbv && (!mask || j <= i)) Cb[i + (size_t)j * g.ldc] = acc[a][b][e];
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = rowA0 + wm * 64 + (h * 4 + a) * 8 + g8;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
-            if (i < g.rows && j < g.rows && i >= j) g.C[i + (size_t)j * g.ldc] = cold[a][b][e] - acc[h * 4 + a][b][e];
-          }
-      }
-    }
-  } else {
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const int i = rowA0 + wm * 64 + a * 8 + g8;
-      if (i >= g.rows) continue;
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = rowB0 + wn * 32 + b * 8 + 2 * t4 + e;
-          if (j < g.cols) g.C[i + (size_t)j * g.ldc] = acc[a][b][e];
-        }
-    }
   }
 }
 
@@ -362,11 +386,13 @@ static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(dou
 static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kNB + 3 * 32 * 33) * sizeof(double); }
 
 template <int MODE>
-static void launch_gemm(bool al16, int grid, const GemmArgs& g, cudaStream_t st) {
-  if (grid <= 0) return;
+static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g, cudaStream_t st) {
+  if (grid.x == 0 || grid.y == 0) return;
   if (al16) gemm_nt_kernel<MODE, true><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
   else gemm_nt_kernel<MODE, false><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
 }
+
+static void set_all_attrs();
 
 template <int MODE>
 static void set_gemm_attr() {
@@ -374,33 +400,71 @@ static void set_gemm_attr() {
   cudaFuncSetAttribute(gemm_nt_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
 }
 
-int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st, double* flops_upd,
-                int* n_upd) {
+// Blocked right-looking Cholesky, outer block width kOuter = 2 * kNB: the trailing updates run with
+// K = 256 (half the C traffic of K = 128); each outer panel is factored as two 128-wide sub-panels.
+constexpr int kOuter = 2 * kNB;
+
+static void set_all_attrs() {
   static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem());
-    set_gemm_attr<kModeTrsm>();
-    set_gemm_attr<kModeSyrkAll>();
-    set_gemm_attr<kModeSyrkCol>();
-    set_gemm_attr<kModeSyrkRest>();
-    attr = true;
-  }
+  if (attr) return;
+  cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem());
+  set_gemm_attr<kModeTrsm>();
+  set_gemm_attr<kModeUpdCols>();
+  set_gemm_attr<kModeUpdTri>();
+  set_gemm_attr<kModeRect>();
+  set_gemm_attr<kModeDist>();
+  attr = true;
+}
+
+static bool aligned16(const void* p, int64_t ld) {
+  return (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(p) & 15) == 0);
+}
+
+int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st, double* flops_upd,
+                int* n_upd, double* linv_ws) {
+  set_all_attrs();
   if (!h->st2) {
     cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&h->evA, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->evB, cudaEventDisableTiming);
   }
   cudaStream_t s2 = h->st2;
-  const bool al16 = (ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+  const bool al16 = aligned16(B, ld);
   const bool tim = h->timing;
   int launches = 0;
   double fl = 0.0;
   int nu = 0;
-  const int64_t nsteps = (m + kNB - 1) / kNB;
-  auto panel = [&](int64_t k, cudaStream_t s) {  // diag(k) + trsm(k)
-    const int64_t k0 = k * kNB;
-    const int kb = (int)std::min<int64_t>(kNB, m - k0);
-    double* Lw = h->potrf_ws + (k & 1) * kNB * kNB;
+  int sub = 0;  // sub-panel counter (Linv double buffer)
+  auto upd = [&](int mode, int64_t kcol, int kw, int64_t base, int c0, int c1, cudaStream_t s) {
+    // B[base:, base:] tile columns [c0, c1) (or [c0, T)) -= B[base:, kcol:kcol+kw] B[base:, kcol:kcol+kw]^T
+    const int rows = (int)(m - base);
+    const int T = (rows + kTile - 1) / kTile;
+    GemmArgs u{};
+    u.A = B + base + (size_t)kcol * ld;
+    u.lda = ld;
+    u.Bm = u.A;
+    u.ldbm = ld;
+    u.C = B + base + (size_t)base * ld;
+    u.ldc = ld;
+    u.rows = rows;
+    u.K = kw;
+    u.c0 = c0;
+    u.c1 = c1;
+    u.err = d_err;
+    int grid = 0;
+    if (mode == kModeUpdCols) {
+      for (int c = c0; c < std::min(c1, T); ++c) grid += T - c;
+      launch_gemm<kModeUpdCols>(al16, dim3(grid), u, s);
+    } else {
+      const int S = T - c0;
+      grid = S > 0 ? S * (S + 1) / 2 : 0;
+      launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s);
+    }
+    if (grid > 0) ++launches;
+    return grid;
+  };
+  auto subpanel = [&](int64_t k0, int kb, cudaStream_t s) {  // diag + trsm of columns [k0, k0+kb)
+    double* Lw = linv_ws + (sub++ & 1) * kNB * kNB;
     potrf_diag_kernel<<<1, kDiagThreads, diag_smem(), s>>>(B, ld, (int)k0, kb, Lw, d_err);
     ++launches;
     const int64_t base = k0 + kb;
@@ -417,36 +481,31 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     g.cols = kb;
     g.K = kb;
     g.err = d_err;
-    launch_gemm<kModeTrsm>(al16, (rows + kTile - 1) / kTile, g, s);
+    launch_gemm<kModeTrsm>(al16, dim3((rows + kTile - 1) / kTile), g, s);
     ++launches;
   };
+  auto panel = [&](int64_t k0, cudaStream_t s) {  // outer block column [k0, k0 + w)
+    const int w = (int)std::min<int64_t>(kOuter, m - k0);
+    subpanel(k0, std::min(kNB, w), s);
+    if (w > kNB) {
+      upd(kModeUpdCols, k0, kNB, k0 + kNB, 0, 1, s);
+      subpanel(k0 + kNB, w - kNB, s);
+    }
+  };
   panel(0, st);
-  for (int64_t k = 0; k < nsteps; ++k) {
-    const int64_t k0 = k * kNB;
-    const int kb = (int)std::min<int64_t>(kNB, m - k0);
-    const int64_t base = k0 + kb;
+  for (int64_t k0 = 0; k0 < m; k0 += kOuter) {
+    const int w = (int)std::min<int64_t>(kOuter, m - k0);
+    const int64_t base = k0 + w;
     const int rows = (int)(m - base);
     if (rows <= 0) break;
-    GemmArgs u{};
-    u.A = B + base + (size_t)k0 * ld;
-    u.lda = ld;
-    u.Bm = u.A;
-    u.ldbm = ld;
-    u.C = B + base + (size_t)base * ld;
-    u.ldc = ld;
-    u.rows = rows;
-    u.cols = kb;
-    u.K = kb;
-    u.err = d_err;
     const int T = (rows + kTile - 1) / kTile;
-    // block column k+1 first, then hand the next panel to the side stream
-    launch_gemm<kModeSyrkCol>(al16, T, u, st);
-    ++launches;
+    const int ncol = std::min<int>(T, kOuter / kTile);  // tile columns of the next outer block column
+    upd(kModeUpdCols, k0, w, base, 0, ncol, st);
     cudaEventRecord(h->evA, st);
     cudaStreamWaitEvent(s2, h->evA, 0);
-    panel(k + 1, s2);
+    panel(base, s2);
     cudaEventRecord(h->evB, s2);
-    if (T > 1) {
+    if (T > ncol) {
       if (tim) {
         if ((int)h->upd_ev.size() < 2 * (nu + 1)) {
           cudaEvent_t e0, e1;
@@ -457,18 +516,86 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
         }
         cudaEventRecord(h->upd_ev[2 * nu], st);
       }
-      launch_gemm<kModeSyrkRest>(al16, (T - 1) * T / 2, u, st);
+      upd(kModeUpdTri, k0, w, base, ncol, 0, st);
       if (tim) cudaEventRecord(h->upd_ev[2 * nu + 1], st);
-      ++launches;
       ++nu;
-      const double r2 = (double)(rows - kTile);
-      fl += r2 * (r2 + 1.0) * (double)kb;
+      // algorithmic flops of this update: the lower triangle of the trailing block past the next
+      // block column (r2 rows), 2 * w flops per entry
+      const double r2 = (double)(rows - ncol * kTile);
+      fl += r2 * (r2 + 1.0) * (double)w;
     }
     cudaStreamWaitEvent(st, h->evB, 0);
   }
   if (flops_upd) *flops_upd = fl;
   if (n_upd) *n_upd = nu;
   return launches;
+}
+
+// A (rows x kb, in place) <- A L^{-T} for the factored kb x kb tile L (kb <= 256) whose 128-block
+// inverses inv[0], inv[1] came from potrf_lower: X1 = A1 L11^{-T}; A2 -= X1 L21^T; X2 = A2 L22^{-T}.
+int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t ldl, const double* inv, int kb,
+               const int32_t* d_err, cudaStream_t st) {
+  set_all_attrs();
+  if (rows <= 0 || kb <= 0) return 0;
+  const bool al16 = aligned16(A, lda) && aligned16(Lt, ldl);
+  const dim3 gr((unsigned)((rows + kTile - 1) / kTile));
+  int launches = 0;
+  GemmArgs g{};
+  g.A = A;
+  g.lda = lda;
+  g.Bm = inv;
+  g.ldbm = kNB;
+  g.C = A;
+  g.ldc = lda;
+  g.rows = (int)rows;
+  g.cols = std::min(kb, kNB);
+  g.K = g.cols;
+  g.err = d_err;
+  launch_gemm<kModeTrsm>(al16, gr, g, st);
+  ++launches;
+  if (kb > kNB) {
+    GemmArgs r = g;
+    r.C = A + (size_t)kNB * lda;
+    r.Bm = Lt + kNB;
+    r.ldbm = ldl;
+    r.cols = kb - kNB;
+    r.K = kNB;
+    launch_gemm<kModeRect>(al16, gr, r, st);
+    GemmArgs t = g;
+    t.C = A + (size_t)kNB * lda;
+    t.A = t.C;
+    t.Bm = inv + kNB * kNB;
+    t.cols = kb - kNB;
+    t.K = kb - kNB;
+    launch_gemm<kModeTrsm>(al16, gr, t, st);
+    launches += 2;
+  }
+  return launches;
+}
+
+// Local trailing update of a 2D block-cyclic Cholesky step: every local tile (I, J) with
+// I >= J, J*nb >= k1 gets C_IJ -= P_I P_J^T (lower part of diagonal tiles), P = the gathered panel
+// (global rows k1.. m, K columns).
+int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1, int K, const Grid& gr, int64_t m,
+                 int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st) {
+  set_all_attrs();
+  if (mloc <= 0 || nloc <= 0 || K <= 0 || k1 >= m) return 0;
+  GemmArgs g{};
+  g.A = P;
+  g.lda = ldp;
+  g.Bm = P;
+  g.ldbm = ldp;
+  g.C = C;
+  g.ldc = ldc;
+  g.K = K;
+  g.g = gr;
+  g.k1 = k1;
+  g.m = m;
+  g.err = d_err;
+  const bool al16 = aligned16(C, ldc) && aligned16(P, ldp);
+  launch_gemm<kModeDist>(al16, dim3((unsigned)((mloc + kTile - 1) / kTile), (unsigned)((nloc + kTile - 1) / kTile)), g,
+                         st);
+  return 1;
 }
 
 }  // namespace sdpc

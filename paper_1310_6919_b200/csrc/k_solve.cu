@@ -6,7 +6,7 @@
 // P:859-869 (reuse of x_p across a column of B; on B200 the whole X-hat fits in HBM, so the
 // columns are materialised once and reused by every column of B, reading #21).
 //
-// Per panel P (columns p0 = 32P .. p0+31, elimination order):
+// Per panel P (RHS vertices rhs[32P .. 32P+31], ascending elimination ids):
 //   forward  L z = E_P  over the union of the etree paths of the panel's columns (ascending
 //            supernodes, whole CTA per supernode; rows off the paths are exactly zero); z <- D^{-1} z;
 //   backward L^T x = z  the top of the tree (big supernodes) one supernode at a time by the whole CTA,
@@ -32,6 +32,7 @@ struct SolveArgs {
   const int64_t* panel_off;
   const int32_t* reach_ptr;
   const int32_t* reach_sn;
+  const int32_t* rhs;  // [npanels * 32] RHS vertex of each slot (elimination id), -1 = padding
   const int32_t* dlev_ptr;
   const int32_t* dlev_sn;
   const int32_t* border;   // backward task order: top supernodes (level order), then subtrees (preorder)
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   const double* __restrict__ Lp = a.Lp[fac];
   const double* __restrict__ D = a.D[fac];
   double* X = a.out[fac] + (size_t)P * n * kPanelW;
-  const int p0 = P * kPanelW;
+  const int myrhs = a.rhs[P * kPanelW + lane];  // this lane's RHS: e_{myrhs} (all-zero column if -1)
   const int32_t* __restrict__ rowind = a.rowind;
 
   const int nwords = (a.nsuper + 31) / 32;
@@ -238,11 +239,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const int r = a.reach_sn[q];
     atomicOr(&inreach[r >> 5], 1u << (r & 31));
   }
-  // initialise z rows on the paths: z[i][lane] = (i == p0 + lane)
+  // initialise z rows on the paths: z[i][lane] = (i == myrhs)
   for (int q = rb + wid; q < re; q += NW) {
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r];
-    for (int t = 0; t < s; ++t) xrow(X, f + t, lane) = (f + t == p0 + lane) ? 1.0 : 0.0;
+    for (int t = 0; t < s; ++t) xrow(X, f + t, lane) = (f + t == myrhs) ? 1.0 : 0.0;
   }
   __syncthreads();
 
@@ -352,6 +353,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.panel_off = h->d.panel_off;
   a.reach_ptr = h->d.reach_ptr;
   a.reach_sn = h->d.reach_sn;
+  a.rhs = h->d.rhs;
   a.dlev_ptr = h->d.dlev_ptr;
   a.dlev_sn = h->d.dlev_sn;
   a.border = h->d.border;
@@ -371,6 +373,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
     cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     attr = true;
   }
+  if (h->d.npanels == 0) return 0;
   dim3 grid(h->d.npanels, 2);
   inverse_panel_kernel<<<grid, kSolveThreads, smem, st>>>(a);
   return 1;

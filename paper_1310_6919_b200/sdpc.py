@@ -21,7 +21,6 @@ _P = C.c_void_p
 _SIGS = [
     ("sdpc_create", C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
                               C.c_int32, _P]),
-    ("sdpc_get_unique_id", C.c_int, [_P]),
     ("sdpc_get_structure", C.c_int, [_P, _P]),
     ("sdpc_get_scm_layout", C.c_int, [_P, _P]),
     ("sdpc_factor_xinv", C.c_int, [_P, _P, _P]),
@@ -30,6 +29,9 @@ _SIGS = [
     ("sdpc_get_y_factor", C.c_int, [_P, _P, _P, _P]),
     ("sdpc_get_inverse_columns", C.c_int, [_P, _P, C.c_int32, _P, _P, _P]),
     ("sdpc_scm_cholesky", C.c_int, [_P, _P, C.c_int64, _P, _P]),
+    ("sdpc_potrf_tile", C.c_int, [_P, _P, C.c_int32, C.c_int64, _P, _P, _P]),
+    ("sdpc_trsm_panel", C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_int32, _P]),
+    ("sdpc_update_tiles", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int32, _P]),
     ("sdpc_iteration_host", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
     ("sdpc_set_timing", C.c_int, [_P, C.c_int32]),
@@ -114,9 +116,9 @@ class Handle:
         self.device = device
 
     @classmethod
-    def from_instance(cls, inst, device=0, with_perm=True):
+    def from_instance(cls, inst, device=0, with_perm=True, nranks=1, rank=0):
         return cls(inst.n, inst.m, inst.a_ptr, inst.a_row, inst.a_col, inst.a_val, inst.b,
-                   inst.perm if with_perm else None, device)
+                   inst.perm if with_perm else None, device, nranks, rank)
 
     def _check(self, st, where):
         if st != SDPC_OK:
@@ -164,6 +166,19 @@ class Handle:
             return int(info.value)
         self._check(st, "sdpc_scm_cholesky")
         return int(info.value)
+
+    # -- distributed SCM Cholesky tile entries (asynchronous; see sdpc.h) --
+    def potrf_tile(self, A, n, lda, inv, info_dev, stream=None):
+        self._check(lib().sdpc_potrf_tile(self.h, _ptr(A), int(n), int(lda), _ptr(inv), _ptr(info_dev),
+                                          _stream(stream)), "sdpc_potrf_tile")
+
+    def trsm_panel(self, A, rows, lda, L, ldl, inv, kb, stream=None):
+        self._check(lib().sdpc_trsm_panel(self.h, _ptr(A), int(rows), int(lda), _ptr(L), int(ldl), _ptr(inv),
+                                          int(kb), _stream(stream)), "sdpc_trsm_panel")
+
+    def update_tiles(self, C_loc, ldc, P, ldp, k1, K, stream=None):
+        self._check(lib().sdpc_update_tiles(self.h, _ptr(C_loc), int(ldc), _ptr(P), int(ldp), int(k1), int(K),
+                                            _stream(stream)), "sdpc_update_tiles")
 
     def iteration_host(self, xbar_E, y_E, rdiag=None, stream=None):
         x = np.ascontiguousarray(xbar_E, dtype=np.float64)

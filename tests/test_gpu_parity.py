@@ -264,3 +264,29 @@ def test_full_config_sampled_columns(cfg):
     R = torch.tril(Bt[:, :m].T)
     res = torch.linalg.norm(BV - R @ (R.T @ V)) / torch.linalg.norm(BV)
     assert float(res) < 1e-13
+
+
+@pytest.mark.parametrize("m", [1, 31, 128, 129, 255, 256, 257, 513, 1000, 1311])
+@pytest.mark.parametrize("pad", [0, 1])
+def test_cholesky_random_spd_ragged(m, pad):
+    """(d) alone: random SPD B of sizes around the 128/256 block edges, even and odd ld (the
+    16-byte and 8-byte staging paths); R against LAPACK potrf; strict upper triangle untouched."""
+    inst, _ = three_by_three()
+    from paper_1310_6919_b200 import Handle
+    h = Handle.from_instance(inst)
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(m * 7 + pad)
+    G = rng.standard_normal((m, m + 8))
+    Bh = G @ G.T / (m + 8) + 0.5 * np.eye(m)
+    ld = m + pad
+    Bt = torch.full((m, ld), float("nan"), dtype=torch.float64, device=dev)   # B(i, j) = Bt[j, i]
+    Bt[:, :m] = torch.from_numpy(np.tril(Bh).T.copy()).to(dev)
+    Bt[:, :m] = torch.where(torch.from_numpy(np.tril(np.ones((m, m))).T.copy()).to(dev) > 0, Bt[:, :m],
+                            torch.tensor(float("nan"), dtype=torch.float64, device=dev))
+    assert h.scm_cholesky(Bt, ld) == 0
+    Rg = Bt[:, :m].T.cpu().numpy()
+    up = np.triu_indices(m, 1)
+    assert np.all(np.isnan(Rg[up]))
+    Ro = CH.potrf_lower(Bh)
+    assert rel(np.tril(Rg), Ro) < TOL_R
+    assert CH.backward_error(Bh, np.tril(Rg)) < 1e-14
