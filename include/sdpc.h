@@ -171,8 +171,8 @@ sdpc_status sdpc_potrf_tile(sdpc_handle h, double* A, int32_t n, int64_t lda, do
                             int32_t* info_dev, void* stream);
 
 /* sdpc_trsm_panel: A (rows x kb, lda >= rows) <- A L^{-T}, L = the kb x kb factored tile
- * (ldl >= kb) and inv its block inverses from sdpc_potrf_tile.  Skipped if this handle's last
- * sdpc_potrf_tile failed. */
+ * (ldl >= kb) and inv its block inverses from sdpc_potrf_tile (a failed tile factorisation is
+ * reported by its info; the later tile calls still run, on meaningless values). */
 sdpc_status sdpc_trsm_panel(sdpc_handle h, double* A, int64_t rows, int64_t lda, const double* L,
                             int64_t ldl, const double* inv, int32_t kb, void* stream);
 

@@ -354,9 +354,15 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   AL(h->Dy, (size_t)n);
   AL(h->upd, (size_t)S.upd_total);
   AL(h->d_err, 1);
+  AL(h->d_ok, 1);
   AL(h->potrf_ws, 2 * 128 * 128);
 #undef AL
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  // error flags start at "no error" (kNoError = bytes 0x7f); d_ok never changes: the distributed
+  // tile kernels run unconditionally (a failed tile factorisation is reported through info)
+  if (cudaMemset(h->d_err, 0x7f, sizeof(int32_t)) != cudaSuccess ||
+      cudaMemset(h->d_ok, 0x7f, sizeof(int32_t)) != cudaSuccess)
+    return fail(SDPC_ERR_CUDA);
   if (cudaGetLastError() != cudaSuccess) return fail(SDPC_ERR_CUDA);
   *out = h;
   return SDPC_OK;
@@ -371,7 +377,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, h->d_ws_off,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
-                  h->d_err, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
+                  h->d_err, h->d_ok, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->pinned_in) cudaFreeHost(h->pinned_in);
@@ -618,7 +624,7 @@ sdpc_status sdpc_trsm_panel(sdpc_handle h, double* A, int64_t rows, int64_t lda,
   if (!h || rows < 0 || kb < 1 || kb > kScmNB || (rows > 0 && (!A || lda < rows)) || !L || ldl < kb || !inv)
     return SDPC_ERR_INVALID_ARG;
   CK(cudaSetDevice(h->device));
-  h->launches += trsm_panel(A, rows, lda, L, ldl, inv, kb, h->d_err, (cudaStream_t)stream);
+  h->launches += trsm_panel(A, rows, lda, L, ldl, inv, kb, h->d_ok, (cudaStream_t)stream);
   CK(cudaGetLastError());
   return SDPC_OK;
 }
@@ -629,7 +635,7 @@ sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const doubl
   if (h->mloc > 0 && h->nloc > 0 && k1 < h->S.m && (!C || !P || ldc < h->mloc || ldp < h->S.m - k1))
     return SDPC_ERR_INVALID_ARG;
   CK(cudaSetDevice(h->device));
-  h->launches += update_tiles(C, ldc, P, ldp, k1, K, h->grid, h->S.m, h->mloc, h->nloc, h->d_err,
+  h->launches += update_tiles(C, ldc, P, ldp, k1, K, h->grid, h->S.m, h->mloc, h->nloc, h->d_ok,
                               (cudaStream_t)stream);
   CK(cudaGetLastError());
   return SDPC_OK;

@@ -97,6 +97,7 @@ struct sdpc_ctx {
   double* Xh = nullptr;          // dense X-hat, panel-major [npanels][n][32]
   double* Yh = nullptr;          // dense Y^{-1}
   int32_t* d_err = nullptr;
+  int32_t* d_ok = nullptr;       // constant kNoError flag (distributed tile kernels)
   double* Bown = nullptr;        // handle-owned B for sdpc_iteration_host
   double* xin = nullptr;         // device staging for sdpc_iteration_host
   double* yin = nullptr;

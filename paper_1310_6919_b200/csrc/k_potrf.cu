@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
         for (int i = 0; i < 32; ++i) {
           double sacc = (i == lane) ? 1.0 : 0.0;
           for (int k = lane; k < i; ++k) sacc -= Ab[i + k * kLdD] * inv32[k][lane];
-          inv32[i][lane] = (i >= lane) ? sacc * __shfl_sync(0xffffffffu, rdiag, i) : 0.0;
+          const double rdi = __shfl_sync(0xffffffffu, rdiag, i);  // every lane: full-mask shuffle
+          inv32[i][lane] = (i >= lane) ? sacc * rdi : 0.0;
           __syncwarp();
         }
       }

@@ -193,12 +193,29 @@ class ThreadComm:
 
 # ----------------------------------------------------------------------------- distributed Cholesky
 
-def dist_cholesky(ops, Bt, L: Layout, comm, dev, stream=None):
+def update_flops(L: Layout, k: int) -> float:
+    """Algorithmic flops of this rank's trailing update at step k (2 * kb per updated entry)."""
+    kb = min(NB, L.m - k * NB)
+    fl = 0.0
+    for I in range(L.myrow, L.nt, L.Pr):
+        if I <= k:
+            continue
+        h = L.tile_rows(I)
+        for J in range(L.mycol, I + 1, L.Pc):
+            if J <= k:
+                continue
+            w = L.tile_rows(J)
+            fl += 2.0 * kb * (h * (h + 1) / 2 if I == J else h * w)
+    return fl
+
+
+def dist_cholesky(ops, Bt, L: Layout, comm, dev, stream=None, timer=None):
     """Factor the distributed SCM in place (lower(B) <- R).  Returns the LAPACK-style info (0 or the
     1-based order of the first non-PD leading minor), identical on every rank.
 
     ops: sdpc Handle (GPU) or a test double with the same potrf_tile / trsm_panel / update_tiles.
     Bt:  local array, torch tensor (nloc, lld), local element (r, c) at Bt[c, r].
+    timer: optional list; gets (start event, end event, algorithmic flops) per local update launch.
     """
     import torch
     m, lld = L.m, L.lld
@@ -254,7 +271,13 @@ def dist_cholesky(ops, Bt, L: Layout, comm, dev, stream=None):
                 src = gathered[pr][:kb * len(tl) * NB].view(kb, len(tl), NB)
                 Pt[:, t0::L.Pr, :].copy_(src)
         # 5: trailing update of my tiles
+        if timer is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         ops.update_tiles(Bt, lld, P, ldp, k1, kb, stream)
+        if timer is not None:
+            e1.record()
+            timer.append((e0, e1, update_flops(L, k)))
     # info: smallest failing global column over all ranks (LAPACK rule)
     loc = torch.full((1,), NO_ERROR, dtype=torch.int64, device=dev)
     bad = (infos != NO_ERROR).nonzero().flatten()
