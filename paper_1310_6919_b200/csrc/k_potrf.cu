@@ -34,16 +34,63 @@ constexpr int kGemmThreads = 256;
 constexpr int kDiagThreads = 256;
 constexpr int kLdD = kNB + 1;  // A[i + j*kLdD]
 
+// Warp-level Cholesky + inverse of a 32 x 32 SPD block (lane = row, the row in registers, columns
+// broadcast by shuffles; every shuffle is executed by all 32 lanes).  In: Ab (shared, ld kLdD),
+// lower part.  Out: Ab lower <- L11; Tinv[i][c] (shared, 32 x 33) <- (L11^{-1})[i][c] (zero above).
+// Returns the failing local column or -1 (uniform over the warp).
+__device__ __noinline__ int warp_chol_inv32(double* Ab, double (*Tinv)[33], int lane) {
+  double row[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * kLdD] : 0.0;
+  int fail = -1;
+  double rinv = 0.0;  // lane j: 1 / L[j][j]
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, row[j], j);
+    if (fail < 0 && !(d > 0.0)) fail = j;
+    const double l = sqrt(d), rl = 1.0 / l;
+    if (lane == j) {
+      row[j] = l;
+      rinv = rl;
+    } else if (lane > j) {
+      row[j] *= rl;
+    }
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, row[j], k);
+      if (lane >= k) row[k] -= row[j] * lkj;
+    }
+  }
+  if (fail >= 0) return fail;
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    if (c <= lane) Ab[lane + c * kLdD] = row[c];
+  __syncwarp();
+  // inverse, lane = column c: x_i = (delta_ic - sum_{k<i} L[i][k] x_k) / L[i][i]
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double acc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) acc -= Ab[i + k * kLdD] * x[k];
+    x[i] = acc * __shfl_sync(0xffffffffu, rinv, i);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Tinv[i][lane] = i >= lane ? x[i] : 0.0;
+  return -1;
+}
+
 __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
   extern __shared__ double sm[];
-  double* A = sm;                  // 128 x 128 (ld 129): lower = L, upper = L^{-T}
-  // current 32-column panel, scaled (P[k][i] = L[i, jb+k]), and scratch for the inverse blocks
+  double* A = sm;  // 128 x 128 (ld 129): lower = L, upper = L^{-T}
+  // current 32-column panel (P[k][i] = L[i, jb+k]) and scratch for the inverse blocks
   double (*P)[kNB] = reinterpret_cast<double (*)[kNB]>(sm + kNB * kLdD);
-  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(sm + kNB * kLdD + 32 * kNB);
-  __shared__ double dL[kNB];
-  const int tid = threadIdx.x;
+  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(sm + kNB * kLdD + 32 * kNB);  // [3]
+  __shared__ double Dinv[4][32][33];  // inverses of the four 32 x 32 diagonal blocks
+  __shared__ int fail_col;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double* Bd = B + k0 + (size_t)k0 * ld;
   for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
     const int i = idx % kNB, j = idx / kNB;
@@ -53,48 +100,14 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     A[i + j * kLdD] = v;
   }
   __syncthreads();
-  // 32-column panels.  (1) warp 0 factors the 32 x 32 diagonal sub-block in registers (lane = row,
-  // shuffles, rsqrt) and inverts it (lane = column, broadcast reads); (2) all threads form the panel
-  // rows below with that inverse; (3) register-tiled trailing update.
-  __shared__ double inv32[32][33];
-  __shared__ int fail_col;
-  const int lane = tid & 31, wid = tid >> 5;
+  // 32-column panels: (1) warp 0 factors + inverts the diagonal block in registers; (2) all threads
+  // form the panel rows below with that inverse (1 x 4 outputs per task); (3) 4 x 4 register-tiled
+  // trailing update.
 #pragma unroll 1
   for (int jb = 0; jb < kNB; jb += 32) {
     if (wid == 0) {
-      // factor the 32 x 32 block in place in shared memory: lane = row jb+lane
-      double* Ab = A + jb + jb * kLdD;  // Ab[i + k*kLdD]
-      int fail = -1;
-      double rdiag = 0.0;
-      for (int j = 0; j < 32; ++j) {
-        const double d = Ab[j + j * kLdD];
-        if (!(d > 0.0)) {  // uniform across the warp
-          fail = j;
-          break;
-        }
-        const double r = rsqrt(d);
-        const double l = Ab[lane + j * kLdD] * r;
-        if (lane == j) rdiag = r;
-        __syncwarp();
-        if (lane >= j) Ab[lane + j * kLdD] = l;
-        __syncwarp();
-        if (lane > j) {
-#pragma unroll 4
-          for (int k = j + 1; k <= lane; ++k) Ab[lane + k * kLdD] -= l * Ab[k + j * kLdD];
-        }
-        __syncwarp();
-      }
-      if (lane == 0) fail_col = fail;
-      if (fail < 0) {
-        // inverse: lane = column c; x_i = (delta_ic - sum_{k<i} L[i][k] x_k) / L[i][i]
-        for (int i = 0; i < 32; ++i) {
-          double sacc = (i == lane) ? 1.0 : 0.0;
-          for (int k = lane; k < i; ++k) sacc -= Ab[i + k * kLdD] * inv32[k][lane];
-          const double rdi = __shfl_sync(0xffffffffu, rdiag, i);  // every lane: full-mask shuffle
-          inv32[i][lane] = (i >= lane) ? sacc * rdi : 0.0;
-          __syncwarp();
-        }
-      }
+      const int f = warp_chol_inv32(A + jb + jb * kLdD, Dinv[jb >> 5], lane);
+      if (lane == 0) fail_col = f;
     }
     __syncthreads();
     if (fail_col >= 0) {
@@ -103,13 +116,19 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     }
     const int r0 = jb + 32, nr = kNB - r0;
     if (nr > 0) {
-      // panel rows below: L[i, jb+c] = sum_{k>=c} A[i, jb+k] Linv[c][k]... (L21 = A21 L11^{-T})
-      for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
-        const int i = r0 + (idx & 31) + (idx >> 10) * 32, c = (idx >> 5) & 31;
-        double acc = 0.0;
+      const double (*Iv)[33] = Dinv[jb >> 5];
+      // L[i, jb+c] = sum_{k <= c} A[i, jb+k] Iv[c][k]; task = (row, 4 columns)
+      for (int t = tid; t < nr * 8; t += kDiagThreads) {
+        const int i = r0 + t % nr, c0 = (t / nr) * 4;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 8
-        for (int k = 0; k <= 31; ++k) acc += A[i + (jb + k) * kLdD] * inv32[c][k];
-        P[c][i] = acc;
+        for (int k = 0; k < 32; ++k) {
+          const double a = A[i + (jb + k) * kLdD];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += a * Iv[c0 + q][k];  // Iv[c][k] = 0 for k > c
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) P[c0 + q][i] = acc[q];
       }
       __syncthreads();
       for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
@@ -153,24 +172,11 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
   // L^{-1}, kept transposed in A's upper triangle: Linv[i][j] at A[j + i*ld] (i >= j).
-  // (1) the four 32 x 32 diagonal blocks: thread (I, c) forward-substitutes column c of block I;
-  // (2) off-diagonal blocks by distance d = I - J: Linv[I,J] = -Linv[I,I] sum_{K=J}^{I-1} L[I,K] Linv[K,J].
-  if (tid < kNB) dL[tid] = A[tid + tid * kLdD];
-  __syncthreads();
-  if (tid < kNB) {
-    const int I = tid >> 5, c = tid & 31, o = I * 32;
-    double* xr = A + (o + c);  // Linv[o+i][o+c] at xr[(o+i) * kLdD]
-    xr[(o + c) * kLdD] = 1.0 / dL[o + c];
-    for (int i = c + 1; i < 32; ++i) {
-      double s0 = 0.0, s1 = 0.0;
-      int k = c;
-      for (; k + 1 < i; k += 2) {
-        s0 += A[(o + i) + (o + k) * kLdD] * xr[(o + k) * kLdD];
-        s1 += A[(o + i) + (o + k + 1) * kLdD] * xr[(o + k + 1) * kLdD];
-      }
-      if (k < i) s0 += A[(o + i) + (o + k) * kLdD] * xr[(o + k) * kLdD];
-      xr[(o + i) * kLdD] = -(s0 + s1) / dL[o + i];
-    }
+  // (1) the diagonal blocks from the warp factorisations; (2) off-diagonal blocks by distance
+  // d = I - J: Linv[I,J] = -Linv[I,I] sum_{K=J}^{I-1} L[I,K] Linv[K,J].
+  for (int idx = tid; idx < 4 * 1024; idx += kDiagThreads) {
+    const int I = idx >> 10, e = idx & 1023, r = e & 31, c = e >> 5;
+    if (r >= c) A[(I * 32 + c) + (I * 32 + r) * kLdD] = Dinv[I][r][c];
   }
   __syncthreads();
   for (int d = 1; d < 4; ++d) {
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
       const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
       const int J = p, I = p + d;
       double acc = 0.0;
-      for (int k = 0; k <= a; ++k) acc -= A[(I * 32 + k) + (I * 32 + a) * kLdD] * T[p][k][b];
+      for (int k = 0; k <= a; ++k) acc -= Dinv[I][a][k] * T[p][k][b];
       A[(J * 32 + b) + (I * 32 + a) * kLdD] = acc;
     }
     __syncthreads();
@@ -384,7 +390,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
 }
 
 static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(double); }
-static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kNB + 3 * 32 * 33) * sizeof(double); }
+static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kNB + 3 * 32 * 33) * sizeof(double); }  // + 34 KB static
 
 template <int MODE>
 static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g, cudaStream_t st) {
@@ -425,7 +431,11 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
                 int* n_upd, double* linv_ws) {
   set_all_attrs();
   if (!h->st2) {
-    cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking);
+    // the lookahead (panel) stream gets the highest priority: its CTAs are scheduled first as the
+    // trailing-update CTAs retire, so the critical path does not queue behind the update
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&h->st2, cudaStreamNonBlocking, hi);
     cudaEventCreateWithFlags(&h->evA, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->evB, cudaEventDisableTiming);
   }

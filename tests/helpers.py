@@ -77,3 +77,13 @@ def small(kind, seed=0):
     if kind == "blockarrow":
         return build("blockarrow", seed=seed, nblk=4, bsz=6, border=3, m=40, name="blockarrow4x6")
     raise ValueError(kind)
+
+
+def scm_handle(m, nranks=1, rank=0):
+    """A handle whose SCM has order m (max-cut on m isolated vertices, A_k = e_k e_k^T), for tests
+    that drive the SCM Cholesky entries on a B of their own."""
+    from paper_1310_6919_b200 import Handle
+    a_ptr = np.arange(m + 2, dtype=np.int64) - 1
+    a_ptr[0] = 0
+    idx = np.arange(m, dtype=np.int32)
+    return Handle(m, m, a_ptr, idx, idx, np.ones(m), np.ones(m), None, 0, nranks, rank)

@@ -19,7 +19,7 @@ torch = pytest.importorskip("torch")
 
 from oracle import cholesky as CH  # noqa: E402
 from paper_1310_6919_b200 import dist as D  # noqa: E402
-from tests.helpers import small  # noqa: E402
+from tests.helpers import scm_handle, small  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -83,7 +83,6 @@ def test_dist_build_writes_own_tiles(kind, P):
 
 
 def _run_threads(m, P, bad=None, seed=0):
-    from paper_1310_6919_b200 import Handle
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(seed)
     G = rng.standard_normal((m, m + 3))
@@ -101,7 +100,7 @@ def _run_threads(m, P, bad=None, seed=0):
         try:
             L = layouts[r]
             torch.cuda.set_device(0)
-            h = _grid_handle(Handle, L)
+            h = scm_handle(L.m, L.P, L.rank)
             ops = h
             Bt = torch.zeros((max(1, L.nloc), L.lld), dtype=torch.float64, device=dev)
             Bt[:L.nloc, :L.mloc] = torch.from_numpy(D.local_tiles_of(np.tril(B), L).T.copy()).to(dev)
@@ -122,16 +121,6 @@ def _run_threads(m, P, bad=None, seed=0):
         t.join(timeout=300)
     assert not errors, errors
     return B, layouts, results
-
-
-def _grid_handle(Handle, L):
-    """A handle whose SCM has order L.m and whose grid is L's: a max-cut problem on m isolated
-    vertices (A_k = e_k e_k^T), so sdpc_update_tiles sees the right m, Pr, Pc, myrow, mycol."""
-    m = L.m
-    a_ptr = np.arange(m + 2, dtype=np.int64) - 1
-    a_ptr[0] = 0
-    idx = np.arange(m, dtype=np.int32)
-    return Handle(m, m, a_ptr, idx, idx, np.ones(m), np.ones(m), None, 0, L.P, L.rank)
 
 
 @pytest.mark.parametrize("m,P", [(700, 2), (1300, 4), (1100, 3), (2100, 8)])

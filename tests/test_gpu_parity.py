@@ -271,9 +271,8 @@ def test_full_config_sampled_columns(cfg):
 def test_cholesky_random_spd_ragged(m, pad):
     """(d) alone: random SPD B of sizes around the 128/256 block edges, even and odd ld (the
     16-byte and 8-byte staging paths); R against LAPACK potrf; strict upper triangle untouched."""
-    inst, _ = three_by_three()
-    from paper_1310_6919_b200 import Handle
-    h = Handle.from_instance(inst)
+    from tests.helpers import scm_handle
+    h = scm_handle(m)
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(m * 7 + pad)
     G = rng.standard_normal((m, m + 8))
