@@ -48,9 +48,9 @@ __device__ __noinline__ int warp_chol_inv32(double* Ab, double (*Tinv)[33], int 
   for (int j = 0; j < 32; ++j) {
     const double d = __shfl_sync(0xffffffffu, row[j], j);
     if (fail < 0 && !(d > 0.0)) fail = j;
-    const double l = sqrt(d), rl = 1.0 / l;
+    const double rl = rsqrt(d);  // one MUFU-seeded op instead of sqrt + divide on the serial chain
     if (lane == j) {
-      row[j] = l;
+      row[j] = d * rl;
       rinv = rl;
     } else if (lane > j) {
       row[j] *= rl;
@@ -66,14 +66,17 @@ __device__ __noinline__ int warp_chol_inv32(double* Ab, double (*Tinv)[33], int 
   for (int c = 0; c < 32; ++c)
     if (c <= lane) Ab[lane + c * kLdD] = row[c];
   __syncwarp();
-  // inverse, lane = column c: x_i = (delta_ic - sum_{k<i} L[i][k] x_k) / L[i][i]
+  // inverse, lane = column c, right-looking (column-oriented) forward substitution: at step i,
+  // x_i is final; it updates every x_k, k > i, independently (ILP across k instead of one serial
+  // dot-product chain per row)
   double x[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double acc = (i == lane) ? 1.0 : 0.0;
+  for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) acc -= Ab[i + k * kLdD] * x[k];
-    x[i] = acc * __shfl_sync(0xffffffffu, rinv, i);
+  for (int i = 0; i < 32; ++i) {
+    x[i] *= __shfl_sync(0xffffffffu, rinv, i);
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) x[k] -= Ab[k + i * kLdD] * x[i];
   }
 #pragma unroll
   for (int i = 0; i < 32; ++i) Tinv[i][lane] = i >= lane ? x[i] : 0.0;
@@ -92,12 +95,20 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
   __shared__ int fail_col;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double* Bd = B + k0 + (size_t)k0 * ld;
-  for (int idx = tid; idx < kNB * kNB; idx += kDiagThreads) {
-    const int i = idx % kNB, j = idx / kNB;
-    double v = 0.0;
-    if (i < kb && j < kb) v = i >= j ? Bd[i + (size_t)j * ld] : 0.0;
-    else if (i == j) v = 1.0;  // identity padding beyond kb
-    A[i + j * kLdD] = v;
+  // load the lower triangle, 16 independent loads in flight per thread
+  for (int base = 0; base < kNB * kNB; base += 16 * kDiagThreads) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = base + q * kDiagThreads + tid;
+      const int i = idx % kNB, j = idx / kNB;
+      v[q] = (i < kb && j < kb && i >= j) ? Bd[i + (size_t)j * ld] : ((i == j && i >= kb) ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = base + q * kDiagThreads + tid;
+      A[idx % kNB + (idx / kNB) * kLdD] = v[q];
+    }
   }
   __syncthreads();
   // 32-column panels: (1) warp 0 factors + inverts the diagonal block in registers; (2) all threads
@@ -171,6 +182,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
+  __syncthreads();  // the diagonal of A is overwritten below (it becomes diag(L^{-1}))
   // L^{-1}, kept transposed in A's upper triangle: Linv[i][j] at A[j + i*ld] (i >= j).
   // (1) the diagonal blocks from the warp factorisations; (2) off-diagonal blocks by distance
   // d = I - J: Linv[I,J] = -Linv[I,I] sum_{K=J}^{I-1} L[I,K] Linv[K,J].
@@ -184,24 +196,25 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
       const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
       const int J = p, I = p + d;
-      double acc0 = 0.0, acc1 = 0.0;
-      // K == J: Linv[J,J] is lower, so only k >= b contributes (the rest of that storage is L)
-      for (int k = b; k < 32; ++k) acc0 += A[(I * 32 + a) + (J * 32 + k) * kLdD] * A[(J * 32 + b) + (J * 32 + k) * kLdD];
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      // K == J: Linv[J,J] is lower, so only k >= b contributes (the rest of that storage is L);
+      // Dinv[J][k][b] = Linv[J,J](k, b), zero for k < b
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc[k & 3] += A[(I * 32 + a) + (J * 32 + k) * kLdD] * Dinv[J][k][b];
       for (int K = J + 1; K < I; ++K)
-#pragma unroll 8
-        for (int k = 0; k < 32; k += 2) {
-          acc0 += A[(I * 32 + a) + (K * 32 + k) * kLdD] * A[(J * 32 + b) + (K * 32 + k) * kLdD];
-          acc1 += A[(I * 32 + a) + (K * 32 + k + 1) * kLdD] * A[(J * 32 + b) + (K * 32 + k + 1) * kLdD];
-        }
-      T[p][a][b] = acc0 + acc1;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          acc[k & 3] += A[(I * 32 + a) + (K * 32 + k) * kLdD] * A[(J * 32 + b) + (K * 32 + k) * kLdD];
+      T[p][a][b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
     __syncthreads();
     for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
       const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
       const int J = p, I = p + d;
-      double acc = 0.0;
-      for (int k = 0; k <= a; ++k) acc -= Dinv[I][a][k] * T[p][k][b];
-      A[(J * 32 + b) + (I * 32 + a) * kLdD] = acc;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc[k & 3] -= Dinv[I][a][k] * T[p][k][b];  // Dinv[I][a][k] = 0 for k > a
+      A[(J * 32 + b) + (I * 32 + a) * kLdD] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
     __syncthreads();
   }
