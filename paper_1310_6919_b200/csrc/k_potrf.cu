@@ -24,15 +24,21 @@
 namespace sdpc {
 
 constexpr int kNB = 128;         // panel width
-constexpr int kTile = 128;       // GEMM tile (BM = BN)
-constexpr int kBK = 16;          // k-chunk per pipeline stage
-constexpr int kStages = 3;
-constexpr int kLdS = kTile + 4;  // smem row stride (doubles): conflict-free fragment loads
-constexpr int kGemmThreads = 256;
+constexpr int kTile = 128;        // GEMM tile rows (BM); also the row/column unit of the tile grids
+constexpr int kBN = 64;           // GEMM tile columns
+constexpr int kBK = 16;           // k-chunk per pipeline stage
+constexpr int kStages = 4;
+constexpr int kLdA = kTile + 4;   // smem row strides (doubles): conflict-free fragment loads
+constexpr int kLdB = kBN + 4;
+constexpr int kGemmThreads = 256;  // 8 warps x (32 x 32), 2 CTAs per SM
+
+__device__ __forceinline__ double neg(double x) {  // sign flip on the integer pipe
+  return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
+}
 
 // ------------------------------------------------------------------ diagonal block
 constexpr int kDiagThreads = 256;
-constexpr int kLdD = kNB + 1;  // A[i + j*kLdD]
+constexpr int kLdD = kNB + 4;  // A[i + j*kLdD]; +4 makes the m8n8k4 fragment loads conflict-free
 
 // Warp-level Cholesky + inverse of a 32 x 32 SPD block (lane = row, the row in registers, columns
 // broadcast by shuffles; every shuffle is executed by all 32 lanes).  In: Ab (shared, ld kLdD),
@@ -83,17 +89,36 @@ __device__ __noinline__ int warp_chol_inv32(double* Ab, double (*Tinv)[33], int 
   return -1;
 }
 
+// One warp: acc (8 x 8 tile, m8n8k4 accumulator layout) += sum_{kk < K} Aop(r0 + row, kk) Bop(c0 + col, kk)
+// with Aop(i, kk) = Ap[i * as_i + kk * as_k], Bop(j, kk) = Bp[j * bs_j + kk * bs_k] (shared memory).
+__device__ __forceinline__ void warp_mma8(double& c0, double& c1, const double* Ap, int as_i, int as_k,
+                                          const double* Bp, int bs_j, int bs_k, int K, bool negA, int lane) {
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const double* ap = Ap + g8 * as_i + t4 * as_k;
+  const double* bp = Bp + g8 * bs_j + t4 * bs_k;
+#pragma unroll 4
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const double av = ap[k0 * as_k];
+    dmma_8x8x4(c0, c1, negA ? neg(av) : av, bp[k0 * bs_k]);
+  }
+}
+
+// Factor the 128 x 128 diagonal block B[k0.., k0..] (kb <= 128 valid, identity-padded) in shared
+// memory and form L11^{-1} for the panel solve.  32-column panels: warp 0 factors + inverts the
+// 32 x 32 diagonal block in registers; the panel rows below (P = A21 L11^{-T}) and the trailing
+// update (A22 -= P P^T) run on the FP64 tensor cores (m8n8k4 DMMA, fragments from shared memory),
+// as do the off-diagonal blocks of L^{-1}.
 __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, int64_t ld, int k0, int kb,
                                                                   double* Linv, int32_t* err) {
   if (*err != kNoError) return;
   extern __shared__ double sm[];
-  double* A = sm;  // 128 x 128 (ld 129): lower = L, upper = L^{-T}
-  // current 32-column panel (P[k][i] = L[i, jb+k]) and scratch for the inverse blocks
-  double (*P)[kNB] = reinterpret_cast<double (*)[kNB]>(sm + kNB * kLdD);
-  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(sm + kNB * kLdD + 32 * kNB);  // [3]
+  double* A = sm;  // 128 x 128 (ld kLdD): lower = L, upper = L^{-T}
+  double* P = sm + kNB * kLdD;  // panel scratch, P[c * kLdD + r] = L[r, jb + c] (32 columns)
+  double (*T)[32][33] = reinterpret_cast<double (*)[32][33]>(sm + kNB * kLdD + 32 * kLdD);  // [3]
   __shared__ double Dinv[4][32][33];  // inverses of the four 32 x 32 diagonal blocks
   __shared__ int fail_col;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
   double* Bd = B + k0 + (size_t)k0 * ld;
   // load the lower triangle, 16 independent loads in flight per thread
   for (int base = 0; base < kNB * kNB; base += 16 * kDiagThreads) {
@@ -111,9 +136,6 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     }
   }
   __syncthreads();
-  // 32-column panels: (1) warp 0 factors + inverts the diagonal block in registers; (2) all threads
-  // form the panel rows below with that inverse (1 x 4 outputs per task); (3) 4 x 4 register-tiled
-  // trailing update.
 #pragma unroll 1
   for (int jb = 0; jb < kNB; jb += 32) {
     if (wid == 0) {
@@ -127,53 +149,37 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     }
     const int r0 = jb + 32, nr = kNB - r0;
     if (nr > 0) {
-      const double (*Iv)[33] = Dinv[jb >> 5];
-      // L[i, jb+c] = sum_{k <= c} A[i, jb+k] Iv[c][k]; task = (row, 4 columns)
-      for (int t = tid; t < nr * 8; t += kDiagThreads) {
-        const int i = r0 + t % nr, c0 = (t / nr) * 4;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-          const double a = A[i + (jb + k) * kLdD];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] += a * Iv[c0 + q][k];  // Iv[c][k] = 0 for k > c
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) P[c0 + q][i] = acc[q];
+      // P(r, c) = sum_k A(r, jb+k) Linv11(c, k): (nr/8) x 4 tiles of 8 x 8, K = 32
+      const double* Iv = &Dinv[jb >> 5][0][0];
+      const int ntile = (nr / 8) * 4;
+      for (int t = wid; t < ntile; t += kDiagThreads / 32) {
+        const int tr = t >> 2, tc = t & 3;
+        double c0 = 0.0, c1 = 0.0;
+        warp_mma8(c0, c1, A + (r0 + tr * 8) + jb * kLdD, 1, kLdD, Iv + tc * 8 * 33, 33, 1, 32, false, lane);
+        const int r = r0 + tr * 8 + g8, c = tc * 8 + 2 * t4;
+        P[c * kLdD + r] = c0;
+        P[(c + 1) * kLdD + r] = c1;
       }
       __syncthreads();
+      // panel back into A (its columns are not touched by the update) and the trailing update
       for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
-        const int c = idx / nr, i = r0 + idx % nr;
-        A[i + (jb + c) * kLdD] = P[c][i];
+        const int c = idx / nr, r = r0 + idx % nr;
+        A[r + (jb + c) * kLdD] = P[c * kLdD + r];
       }
-      // trailing update of rows/cols >= r0 with the panel: 4 x 4 register tiles
-      const int nb4 = nr / 4;
-      const int ntile = nb4 * (nb4 + 1) / 2;
-      for (int t = tid; t < ntile; t += kDiagThreads) {
-        int bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-        while (bi * (bi + 1) / 2 > t) --bi;
-        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-        const int bj = t - bi * (bi + 1) / 2;
-        const int i0 = r0 + 4 * bi, j0 = r0 + 4 * bj;
-        double acc[4][4] = {};
-#pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-          double pi[4], pj[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            pi[q] = P[k][i0 + q];
-            pj[q] = P[k][j0 + q];
-          }
-#pragma unroll
-          for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-            for (int b2 = 0; b2 < 4; ++b2) acc[a2][b2] += pi[a2] * pj[b2];
-        }
-#pragma unroll
-        for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-          for (int b2 = 0; b2 < 4; ++b2)
-            if (i0 + a2 >= j0 + b2) A[(i0 + a2) + (j0 + b2) * kLdD] -= acc[a2][b2];
+      // A22 -= P P^T on the 8 x 8 tiles (ti >= tj) of rows/cols r0..127 (the strict upper part of
+      // the diagonal tiles is scratch: overwritten by L^{-T} below, never read as L)
+      const int nb8 = nr / 8, nt2 = nb8 * (nb8 + 1) / 2;
+      for (int t = wid; t < nt2; t += kDiagThreads / 32) {
+        int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while (ti * (ti + 1) / 2 > t) --ti;
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int i0 = r0 + ti * 8, j0 = r0 + tj * 8;
+        double* Cp = A + (i0 + g8) + (j0 + 2 * t4) * kLdD;
+        double c0 = Cp[0], c1 = Cp[kLdD];
+        warp_mma8(c0, c1, P + i0, 1, kLdD, P + j0, 1, kLdD, 32, true, lane);
+        Cp[0] = c0;
+        Cp[kLdD] = c1;
       }
     }
     __syncthreads();
@@ -182,10 +188,10 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
   }
-  __syncthreads();  // the diagonal of A is overwritten below (it becomes diag(L^{-1}))
+  __syncthreads();  // the upper triangle (and diagonal) of A is overwritten below with L^{-T}
   // L^{-1}, kept transposed in A's upper triangle: Linv[i][j] at A[j + i*ld] (i >= j).
   // (1) the diagonal blocks from the warp factorisations; (2) off-diagonal blocks by distance
-  // d = I - J: Linv[I,J] = -Linv[I,I] sum_{K=J}^{I-1} L[I,K] Linv[K,J].
+  // d = I - J: T = sum_{K=J}^{I-1} L[I,K] Linv[K,J]; Linv[I,J] = -Linv[I,I] T (DMMA 8 x 8 tiles).
   for (int idx = tid; idx < 4 * 1024; idx += kDiagThreads) {
     const int I = idx >> 10, e = idx & 1023, r = e & 31, c = e >> 5;
     if (r >= c) A[(I * 32 + c) + (I * 32 + r) * kLdD] = Dinv[I][r][c];
@@ -193,28 +199,29 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
   __syncthreads();
   for (int d = 1; d < 4; ++d) {
     const int npair = 4 - d;
-    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
-      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
-      const int J = p, I = p + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      // K == J: Linv[J,J] is lower, so only k >= b contributes (the rest of that storage is L);
-      // Dinv[J][k][b] = Linv[J,J](k, b), zero for k < b
-#pragma unroll
-      for (int k = 0; k < 32; ++k) acc[k & 3] += A[(I * 32 + a) + (J * 32 + k) * kLdD] * Dinv[J][k][b];
-      for (int K = J + 1; K < I; ++K)
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          acc[k & 3] += A[(I * 32 + a) + (K * 32 + k) * kLdD] * A[(J * 32 + b) + (K * 32 + k) * kLdD];
-      T[p][a][b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    for (int t = wid; t < npair * 16; t += kDiagThreads / 32) {
+      const int pp = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
+      const int J = pp, I = pp + d;
+      double c0 = 0.0, c1 = 0.0;
+      // K = J: Linv[J,J] from Dinv (lower); Bop(b, k) = Dinv[J][k][b]
+      warp_mma8(c0, c1, A + (I * 32 + tr * 8) + (J * 32) * kLdD, 1, kLdD, &Dinv[J][0][tc * 8], 1, 33, 32, false,
+                lane);
+      for (int K = J + 1; K < I; ++K)  // Bop(b, k) = Linv[K32+k][J32+b] = A[(J32+b) + (K32+k) ld]
+        warp_mma8(c0, c1, A + (I * 32 + tr * 8) + (K * 32) * kLdD, 1, kLdD, A + (J * 32 + tc * 8) + (K * 32) * kLdD,
+                  1, kLdD, 32, false, lane);
+      T[pp][tr * 8 + g8][tc * 8 + 2 * t4] = c0;
+      T[pp][tr * 8 + g8][tc * 8 + 2 * t4 + 1] = c1;
     }
     __syncthreads();
-    for (int idx = tid; idx < npair * 1024; idx += kDiagThreads) {
-      const int p = idx >> 10, e = idx & 1023, a = e & 31, b = e >> 5;
-      const int J = p, I = p + d;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < 32; ++k) acc[k & 3] -= Dinv[I][a][k] * T[p][k][b];  // Dinv[I][a][k] = 0 for k > a
-      A[(J * 32 + b) + (I * 32 + a) * kLdD] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    for (int t = wid; t < npair * 16; t += kDiagThreads / 32) {
+      const int pp = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
+      const int J = pp, I = pp + d;
+      double c0 = 0.0, c1 = 0.0;
+      // Linv[I,J](a, b) = -sum_k Dinv[I][a][k] T[k][b]
+      warp_mma8(c0, c1, &Dinv[I][tr * 8][0], 33, 1, &T[pp][0][tc * 8], 1, 33, 32, true, lane);
+      const int a = tr * 8 + g8, b = tc * 8 + 2 * t4;
+      A[(J * 32 + b) + (I * 32 + a) * kLdD] = c0;
+      A[(J * 32 + b + 1) + (I * 32 + a) * kLdD] = c1;
     }
     __syncthreads();
   }
@@ -249,94 +256,103 @@ struct GemmArgs {
 
 enum { kModeTrsm = 0, kModeUpdCols = 1, kModeUpdTri = 2, kModeRect = 3, kModeDist = 4 };
 
-__device__ __forceinline__ double neg(double x) {  // sign flip on the integer pipe
-  return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
-}
 
 template <int MODE, bool AL16>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, 2) gemm_nt_kernel(GemmArgs g) {
   if (*g.err != kNoError) return;
   extern __shared__ double sm[];
-  double* As = sm;                         // [kStages][kBK][kLdS]
-  double* Bs = sm + kStages * kBK * kLdS;  // [kStages][kBK][kLdS]
+  double* As = sm;                          // [kStages][kBK][kLdA]
+  double* Bs = sm + kStages * kBK * kLdA;   // [kStages][kBK][kLdB]
   constexpr bool UPD = MODE != kModeTrsm;
-  // tile -> operand bases, valid extents, and whether the tile straddles the diagonal (mask j > i)
+  // tile (128 rows x 64 columns) -> operand bases, valid extents, diagonal mask (column j of the
+  // tile is global column i0 + doff + j when row i is global row i0 + i; keep j + doff <= i)
   const double* Ab;
   const double* Bb;
   double* Cb;
-  int na, nbv;
+  int na, nbv, doff = 0;
   bool mask;
   if (MODE == kModeTrsm || MODE == kModeRect) {
     const int bi = blockIdx.x, bj = blockIdx.y;
     Ab = g.A + (size_t)bi * kTile;
-    Bb = g.Bm + (size_t)bj * kTile;
-    Cb = g.C + (size_t)bi * kTile + (size_t)bj * kTile * g.ldc;
+    Bb = g.Bm + (size_t)bj * kBN;
+    Cb = g.C + (size_t)bi * kTile + (size_t)bj * kBN * g.ldc;
     na = g.rows - bi * kTile;
-    nbv = g.cols - bj * kTile;
+    nbv = g.cols - bj * kBN;
     mask = false;
   } else if (MODE == kModeDist) {
-    const int64_t la = (int64_t)blockIdx.x * kTile, lb = (int64_t)blockIdx.y * kTile;
+    const int64_t la = (int64_t)blockIdx.x * kTile, lb = (int64_t)blockIdx.y * kBN;
     const int64_t gi = ((la / kScmNB) * g.g.Pr + g.g.pr) * kScmNB + la % kScmNB;
     const int64_t gj = ((lb / kScmNB) * g.g.Pc + g.g.pc) * kScmNB + lb % kScmNB;
-    if (gj < g.k1 || gi < gj || gi >= g.m) return;
+    if (gj < g.k1 || gi + kTile <= gj || gi >= g.m) return;
     Ab = g.A + (gi - g.k1);
     Bb = g.A + (gj - g.k1);
     Cb = g.C + la + lb * g.ldc;
     na = (int)(g.m - gi < kTile ? g.m - gi : kTile);
-    nbv = (int)(g.m - gj < kTile ? g.m - gj : kTile);
-    mask = gi == gj;
+    nbv = (int)(g.m - gj < kBN ? g.m - gj : kBN);
+    doff = (int)(gj - gi);
+    mask = gj + kBN > gi;
   } else {
     const int T = (g.rows + kTile - 1) / kTile;
-    int t = blockIdx.x, bi, bj;
-    if (MODE == kModeUpdCols) {  // column-major over the few columns [c0, c1)
-      bj = g.c0;
-      while (t >= T - bj) {
-        t -= T - bj;
-        ++bj;
+    int t = blockIdx.x, bi, bj;  // bj in 64-column units
+    if (MODE == kModeUpdCols) {  // column-major over the 128-columns [c0, c1), two halves each
+      int c = g.c0;
+      while (t >= 2 * (T - c)) {
+        t -= 2 * (T - c);
+        ++c;
       }
-      bi = bj + t;
-    } else {  // row-major over the lower triangle of tile columns [c0, T)
-      int r = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-      while (r * (r + 1) / 2 > t) --r;
-      while ((r + 1) * (r + 2) / 2 <= t) ++r;
+      bi = c + (t >> 1);
+      bj = 2 * c + (t & 1);
+    } else {  // row-major over the lower triangle of 128-columns [c0, T): row r has 2r + 2 halves
+      int r = (int)((sqrt(4.0 * t + 1.0) - 1.0) * 0.5);
+      while (r * (r + 1) > t) --r;
+      while ((r + 1) * (r + 2) <= t) ++r;
       bi = g.c0 + r;
-      bj = g.c0 + t - r * (r + 1) / 2;
+      bj = 2 * g.c0 + (t - r * (r + 1));
     }
     Ab = g.A + (size_t)bi * kTile;
-    Bb = g.Bm + (size_t)bj * kTile;
-    Cb = g.C + (size_t)bi * kTile + (size_t)bj * kTile * g.ldc;
+    Bb = g.Bm + (size_t)bj * kBN;
+    Cb = g.C + (size_t)bi * kTile + (size_t)bj * kBN * g.ldc;
     na = g.rows - bi * kTile;
-    nbv = g.rows - bj * kTile;
-    mask = bi == bj;
+    nbv = g.rows - bj * kBN;
+    doff = bj * kBN - bi * kTile;
+    mask = doff + kBN > 0;
   }
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int wm = wid >> 2, wn = wid & 3;  // 2 x 4 warps, warp tile 64 x 32
+  const int wm = wid & 3, wn = wid >> 2;  // 4 x 2 warps, warp tile 32 x 32
   const int g8 = lane >> 2, t4 = lane & 3;
 
   auto load_stage = [&](int stage, int k0) {
-    double* as = As + stage * kBK * kLdS;
-    double* bs = Bs + stage * kBK * kLdS;
+    double* as = As + stage * kBK * kLdA;
+    double* bs = Bs + stage * kBK * kLdB;
     if (AL16) {
 #pragma unroll
       for (int q = 0; q < (kBK * kTile / 2) / kGemmThreads; ++q) {  // 16B chunks: 2 rows of one column
         const int cid = tid + q * kGemmThreads;
         const int kk = cid / (kTile / 2), rp = (cid % (kTile / 2)) * 2;
-        const bool kv = (k0 + kk) < g.K;
-        const bool va = kv && rp < na;
-        cp_async16(as + kk * kLdS + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
-        const bool vb = kv && rp < nbv;
-        cp_async16(bs + kk * kLdS + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
+        const bool va = (k0 + kk) < g.K && rp < na;
+        cp_async16(as + kk * kLdA + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
+      }
+#pragma unroll
+      for (int q = 0; q < (kBK * kBN / 2) / kGemmThreads; ++q) {
+        const int cid = tid + q * kGemmThreads;
+        const int kk = cid / (kBN / 2), rp = (cid % (kBN / 2)) * 2;
+        const bool vb = (k0 + kk) < g.K && rp < nbv;
+        cp_async16(bs + kk * kLdB + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
       }
     } else {
 #pragma unroll
       for (int q = 0; q < (kBK * kTile) / kGemmThreads; ++q) {  // 8B elements
         const int cid = tid + q * kGemmThreads;
         const int kk = cid / kTile, rp = cid % kTile;
-        const bool kv = (k0 + kk) < g.K;
-        const bool va = kv && rp < na;
-        cp_async8(as + kk * kLdS + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
-        const bool vb = kv && rp < nbv;
-        cp_async8(bs + kk * kLdS + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
+        const bool va = (k0 + kk) < g.K && rp < na;
+        cp_async8(as + kk * kLdA + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
+      }
+#pragma unroll
+      for (int q = 0; q < (kBK * kBN) / kGemmThreads; ++q) {
+        const int cid = tid + q * kGemmThreads;
+        const int kk = cid / kBN, rp = cid % kBN;
+        const bool vb = (k0 + kk) < g.K && rp < nbv;
+        cp_async8(bs + kk * kLdB + rp, vb ? Bb + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
       }
     }
   };
@@ -348,17 +364,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
     cp_async_commit();
   }
 
-  // accumulators: C (updates; lower part only of a diagonal tile) or zero (TRSM)
-  double acc[8][4][2];
+  // accumulators: C (updates; lower part only where the tile meets the diagonal) or zero (TRSM)
+  double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int i = wm * 64 + a * 8 + g8;
+  for (int a = 0; a < 4; ++a) {
+    const int i = wm * 32 + a * 8 + g8;
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = wn * 32 + b * 8 + 2 * t4 + e;
-        acc[a][b][e] = (UPD && i < na && j < nbv && (!mask || j <= i)) ? Cb[i + (size_t)j * g.ldc] : 0.0;
+        acc[a][b][e] = (UPD && i < na && j < nbv && (!mask || j + doff <= i)) ? Cb[i + (size_t)j * g.ldc] : 0.0;
       }
   }
 
@@ -368,18 +384,105 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
     const int nxt = kc + kStages - 1;
     if (nxt < nk) load_stage(nxt % kStages, nxt * kBK);
     cp_async_commit();
-    const double* as = As + (kc % kStages) * kBK * kLdS;
-    const double* bs = Bs + (kc % kStages) * kBK * kLdS;
+    const double* as = As + (kc % kStages) * kBK * kLdA;
+    const double* bs = Bs + (kc % kStages) * kBK * kLdB;
+#pragma unroll
+    for (int k4 = 0; k4 < kBK / 4; ++k4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double v = as[(k4 * 4 + t4) * kLdA + wm * 32 + a * 8 + g8];
+        af[a] = UPD ? neg(v) : v;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = bs[(k4 * 4 + t4) * kLdB + wn * 32 + b * 8 + g8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = wm * 32 + a * 8 + g8;
+    if (i >= na) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = wn * 32 + b * 8 + 2 * t4 + e;
+        if (j < nbv && (!mask || j + doff <= i)) Cb[i + (size_t)j * g.ldc] = acc[a][b][e];
+      }
+  }
+}
+
+// In-place panel solve C = A B^T (C == A allowed: each CTA reads all K columns of its 128 rows
+// before writing any of them, and owns all <= 128 output columns of those rows).  128 x 128 tile,
+// 8 warps x (64 x 32), same pipeline as the update kernel.
+template <bool AL16>
+__global__ void __launch_bounds__(kGemmThreads, 1) trsm_kernel(GemmArgs g) {
+  if (*g.err != kNoError) return;
+  extern __shared__ double sm[];
+  double* As = sm;                          // [kStages][kBK][kLdA]
+  double* Bs = sm + kStages * kBK * kLdA;   // [kStages][kBK][kLdA]
+  const int bi = blockIdx.x;
+  const double* Ab = g.A + (size_t)bi * kTile;
+  double* Cb = g.C + (size_t)bi * kTile;
+  const int na = g.rows - bi * kTile, nbv = g.cols;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wm = wid >> 2, wn = wid & 3;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  auto load_stage = [&](int stage, int k0) {
+    double* as = As + stage * kBK * kLdA;
+    double* bs = Bs + stage * kBK * kLdA;
+#pragma unroll
+    for (int q = 0; q < (kBK * kTile) / kGemmThreads; ++q) {
+      const int cid = tid + q * kGemmThreads;
+      const int kk = cid / kTile, rp = cid % kTile;
+      const bool kv = (k0 + kk) < g.K;
+      if (AL16) {
+        if ((rp & 1) == 0) {
+          const bool va = kv && rp < na;
+          cp_async16(as + kk * kLdA + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
+          const bool vb = kv && rp < nbv;
+          cp_async16(bs + kk * kLdA + rp, vb ? g.Bm + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
+        }
+      } else {
+        const bool va = kv && rp < na;
+        cp_async8(as + kk * kLdA + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
+        const bool vb = kv && rp < nbv;
+        cp_async8(bs + kk * kLdA + rp, vb ? g.Bm + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
+      }
+    }
+  };
+  const int nk = (g.K + kBK - 1) / kBK;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nk) load_stage(s, s * kBK);
+    cp_async_commit();
+  }
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    const int nxt = kc + kStages - 1;
+    if (nxt < nk) load_stage(nxt % kStages, nxt * kBK);
+    cp_async_commit();
+    const double* as = As + (kc % kStages) * kBK * kLdA;
+    const double* bs = Bs + (kc % kStages) * kBK * kLdA;
 #pragma unroll
     for (int k4 = 0; k4 < kBK / 4; ++k4) {
       double af[8], bf[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        const double v = as[(k4 * 4 + t4) * kLdS + wm * 64 + a * 8 + g8];
-        af[a] = UPD ? neg(v) : v;
-      }
+      for (int a = 0; a < 8; ++a) af[a] = as[(k4 * 4 + t4) * kLdA + wm * 64 + a * 8 + g8];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = bs[(k4 * 4 + t4) * kLdS + wn * 32 + b * 8 + g8];
+      for (int b = 0; b < 4; ++b) bf[b] = bs[(k4 * 4 + t4) * kLdA + wn * 32 + b * 8 + g8];
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
@@ -387,7 +490,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
     }
   }
   cp_async_wait<0>();
-
+  __syncthreads();  // every warp of this CTA has read its A rows before any is overwritten
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
     const int i = wm * 64 + a * 8 + g8;
@@ -397,17 +500,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_nt_kernel(GemmArgs g) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = wn * 32 + b * 8 + 2 * t4 + e;
-        if (j < nbv && (!mask || j <= i)) Cb[i + (size_t)j * g.ldc] = acc[a][b][e];
+        if (j < nbv) Cb[i + (size_t)j * g.ldc] = acc[a][b][e];
       }
   }
 }
 
-static size_t gemm_smem() { return (size_t)2 * kStages * kBK * kLdS * sizeof(double); }
-static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kNB + 3 * 32 * 33) * sizeof(double); }  // + 34 KB static
+static size_t trsm_smem() { return (size_t)2 * kStages * kBK * kLdA * sizeof(double); }
+
+static size_t gemm_smem() { return (size_t)kStages * kBK * (kLdA + kLdB) * sizeof(double); }
+static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kLdD + 3 * 32 * 33) * sizeof(double); }  // + 34 KB static
 
 template <int MODE>
 static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g, cudaStream_t st) {
   if (grid.x == 0 || grid.y == 0) return;
+  if (MODE == kModeTrsm) {  // in place: one CTA owns all (<= 128) columns of its rows
+    if (al16) trsm_kernel<true><<<dim3(grid.x), kGemmThreads, trsm_smem(), st>>>(g);
+    else trsm_kernel<false><<<dim3(grid.x), kGemmThreads, trsm_smem(), st>>>(g);
+    return;
+  }
   if (al16) gemm_nt_kernel<MODE, true><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
   else gemm_nt_kernel<MODE, false><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
 }
@@ -428,7 +538,8 @@ static void set_all_attrs() {
   static bool attr = false;
   if (attr) return;
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem());
-  set_gemm_attr<kModeTrsm>();
+  cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem());
+  cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem());
   set_gemm_attr<kModeUpdCols>();
   set_gemm_attr<kModeUpdTri>();
   set_gemm_attr<kModeRect>();
@@ -477,11 +588,11 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     u.err = d_err;
     int grid = 0;
     if (mode == kModeUpdCols) {
-      for (int c = c0; c < std::min(c1, T); ++c) grid += T - c;
+      for (int c = c0; c < std::min(c1, T); ++c) grid += 2 * (T - c);
       launch_gemm<kModeUpdCols>(al16, dim3(grid), u, s);
     } else {
       const int S = T - c0;
-      grid = S > 0 ? S * (S + 1) / 2 : 0;
+      grid = S > 0 ? S * (S + 1) : 0;
       launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s);
     }
     if (grid > 0) ++launches;
@@ -584,7 +695,7 @@ int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t l
     r.ldbm = ldl;
     r.cols = kb - kNB;
     r.K = kNB;
-    launch_gemm<kModeRect>(al16, gr, r, st);
+    launch_gemm<kModeRect>(al16, dim3(gr.x, (unsigned)((r.cols + kBN - 1) / kBN)), r, st);
     GemmArgs t = g;
     t.C = A + (size_t)kNB * lda;
     t.A = t.C;
@@ -617,7 +728,7 @@ int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k
   g.m = m;
   g.err = d_err;
   const bool al16 = aligned16(C, ldc) && aligned16(P, ldp);
-  launch_gemm<kModeDist>(al16, dim3((unsigned)((mloc + kTile - 1) / kTile), (unsigned)((nloc + kTile - 1) / kTile)), g,
+  launch_gemm<kModeDist>(al16, dim3((unsigned)((mloc + kTile - 1) / kTile), (unsigned)((nloc + kBN - 1) / kBN)), g,
                          st);
   return 1;
 }
