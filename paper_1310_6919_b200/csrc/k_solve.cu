@@ -101,98 +101,168 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
   }
 }
 
-// ---- CTA-cooperative pieces (all warps, CTA barriers), rows staged in shared memory ----
-constexpr int kStageRows = 384;  // rows of 256 B staged per CTA (96 KB)
+// ---- big supernodes (|S_r| >= kBigS): whole CTA, FP64 tensor cores (m8n8k4 DMMA) -------------
+// The rectangular parts of both sweeps are small GEMMs whose operands come straight from L2:
+// A = a block of the supernode panel L_r, B = 8-RHS slices of gathered rows of the panel X, so
+// every warp task is one 8 x 8 output tile (8 rows of the supernode x 8 RHS) with K running over
+// the panel rows / columns.  The triangular L_SS parts run on 128-row chunks staged in shared
+// memory (16-row diagonal blocks in registers of one warp, the rest of the chunk by all warps).
+constexpr int kBigS = 16;     // supernodes with at least this many columns take this path
+constexpr int kChunk = 128;   // rows of S per shared-memory chunk
+constexpr int kVs = 36;       // chunk row stride (doubles): conflict-free 8-RHS fragment reads
 
-// stage rows S (zero if !s_valid) then U of a supernode into R[0..s+u) with cp.async
-__device__ __forceinline__ void stage_rows(double* R, const double* X, int f, int s, const int32_t* __restrict__ U,
-                                           int u, bool s_valid, int tid, int nt) {
-  for (int idx = tid; idx < (s + u) * 16; idx += nt) {
-    const int row = idx >> 4, ch = idx & 15;
-    const int src = row < s ? f + row : U[row - s];
-    const bool v = row < s ? s_valid : true;
-    cp_async16(R + row * kPanelW + ch * 2, X + (size_t)src * kPanelW + ch * 2, v);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
+// row of X holding the k-th operand row of a gather: f + k for k < s (rows S), U[k - s] after
+__device__ __forceinline__ int op_row(int k, int f, int s, const int32_t* __restrict__ U) {
+  return k < s ? f + k : U[k - s];
 }
 
-// backward for a staged supernode: R[t] = y_t - sum_q L[s+q,t] R[s+q]; then x[S] = L_SS^{-T} R[S]
-__device__ __forceinline__ void coop_bwd_staged(const double* __restrict__ Lr, int c, int s, double* R, int lane,
-                                                int wid, int nw) {
-  const int u = c - s;
-  for (int t = wid; t < s; t += nw) {
-    const double* Lt = Lr + s + (size_t)t * c;
-    double a0 = R[t * kPanelW + lane], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int q = 0;
-    for (; q + 3 < u; q += 4) {
-      a0 -= Lt[q] * R[(s + q) * kPanelW + lane];
-      a1 -= Lt[q + 1] * R[(s + q + 1) * kPanelW + lane];
-      a2 -= Lt[q + 2] * R[(s + q + 2) * kPanelW + lane];
-      a3 -= Lt[q + 3] * R[(s + q + 3) * kPanelW + lane];
-    }
-    for (; q < u; ++q) a0 -= Lt[q] * R[(s + q) * kPanelW + lane];
-    R[t * kPanelW + lane] = (a0 + a1) + (a2 + a3);
+// One warp, one 8 x 8 tile: (c0, c1) += sum_{k < K} A(t, k) X[row(kb0 + k)][n0 + n] with
+// A(t, k) = Ab[t * as_t + k * as_k] for t < nt (zero beyond), rows gathered by op_row.
+__device__ __forceinline__ void tile_gemm_gather(double& c0, double& c1, const double* __restrict__ Ab, int as_t,
+                                                 int as_k, int nt, const double* X, int kb0, int K, int f, int s,
+                                                 const int32_t* __restrict__ U, int n0, int lane) {
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const bool tv = g8 < nt;
+  const double* ap = Ab + (size_t)g8 * as_t + (size_t)t4 * as_k;
+#pragma unroll 2
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const int k = k0 + t4;
+    const bool kv = k < K;
+    const double av = (tv && kv) ? ap[(size_t)k0 * as_k] : 0.0;
+    const double bv = kv ? X[(size_t)op_row(kb0 + k, f, s, U) * kPanelW + n0 + g8] : 0.0;
+    dmma_8x8x4(c0, c1, av, bv);
   }
-  __syncthreads();
-  for (int t1 = s; t1 > 0; t1 -= 16) {
-    const int t0 = t1 > 16 ? t1 - 16 : 0;
-    if (wid == 0) {
-      for (int t = t1 - 1; t >= t0; --t) {
-        double v = R[t * kPanelW + lane];
-        for (int tp = t + 1; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * R[tp * kPanelW + lane];
-        R[t * kPanelW + lane] = v;
+}
+
+// forward, big supernode r: z[S] = L_SS^{-1} z[S] (chunks ascending), then z[U] -= L_US z[S]
+__device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, const int32_t* __restrict__ U,
+                        double* X, double* Vs, int tid, int lane, int wid, int nw) {
+  const int g8 = lane >> 2, t4 = lane & 3;
+  for (int t0 = 0; t0 < s; t0 += kChunk) {
+    const int w = min(kChunk, s - t0);
+    // V = z[S_c] - L[S_c, S_<c] z[S_<c]   (tile tasks: (w/8) x 4)
+    const int ntt = (w + 7) >> 3;
+    for (int task = wid; task < ntt * 4; task += nw) {
+      const int tt = task >> 2, n0 = (task & 3) * 8;
+      const int r0 = tt * 8 + g8;
+      double c0 = 0.0, c1 = 0.0;
+      if (r0 < w) {
+        c0 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4];
+        c1 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4 + 1];
+      }
+      if (t0 > 0) {
+        // A(t, k) = L[t0 + tt*8 + t][k]: as_t = 1, as_k = c; negated through the B operand sign
+        double d0 = 0.0, d1 = 0.0;
+        tile_gemm_gather(d0, d1, Lr + t0 + tt * 8, 1, c, min(8, w - tt * 8), X, 0, t0, f, s, U, n0, lane);
+        c0 -= d0;
+        c1 -= d1;
+      }
+      if (r0 < w) {
+        Vs[r0 * kVs + n0 + 2 * t4] = c0;
+        Vs[r0 * kVs + n0 + 2 * t4 + 1] = c1;
       }
     }
     __syncthreads();
-    for (int t = wid; t < t0; t += nw) {
-      double v = R[t * kPanelW + lane];
-      for (int tp = t0; tp < t1; ++tp) v -= Lr[tp + (size_t)t * c] * R[tp * kPanelW + lane];
-      R[t * kPanelW + lane] = v;
+    // chunk triangle, 16-row diagonal blocks
+    for (int b0 = 0; b0 < w; b0 += 16) {
+      const int bw = min(16, w - b0);
+      if (wid == 0) {
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = j < bw ? Vs[(b0 + j) * kVs + lane] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+#pragma unroll
+          for (int jj = j + 1; jj < 16; ++jj)
+            if (jj < bw) acc[jj] -= Lr[(t0 + b0 + jj) + (size_t)(t0 + b0 + j) * c] * acc[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < bw) Vs[(b0 + j) * kVs + lane] = acc[j];
+      }
+      __syncthreads();
+      for (int t = b0 + bw + wid; t < w; t += nw) {
+        double v = Vs[t * kVs + lane];
+        for (int j = 0; j < bw; ++j) v -= Lr[(t0 + t) + (size_t)(t0 + b0 + j) * c] * Vs[(b0 + j) * kVs + lane];
+        Vs[t * kVs + lane] = v;
+      }
+      __syncthreads();
     }
+    for (int t = wid; t < w; t += nw) X[(size_t)(f + t0 + t) * kPanelW + lane] = Vs[t * kVs + lane];
     __syncthreads();
+  }
+  // z[U] -= L_US z[S]: tile tasks (u/8) x 4, C = gathered rows of X (read-modify-write)
+  const int u = c - s;
+  const int nqt = (u + 7) >> 3;
+  for (int task = wid; task < nqt * 4; task += nw) {
+    const int qt = task >> 2, n0 = (task & 3) * 8;
+    const int q = qt * 8 + g8;
+    double d0 = 0.0, d1 = 0.0;
+    tile_gemm_gather(d0, d1, Lr + s + qt * 8, 1, c, min(8, u - qt * 8), X, 0, s, f, s, U, n0, lane);
+    if (q < u) {
+      double* xr = X + (size_t)U[q] * kPanelW + n0 + 2 * t4;
+      xr[0] -= d0;
+      xr[1] -= d1;
+    }
   }
 }
 
-// forward triangle on staged S rows: R[S] = L_SS^{-1} R[S] (unit lower), blocked by 16
-__device__ __forceinline__ void coop_fwd_tri_staged(const double* __restrict__ Lr, int c, int s, double* R, int lane,
-                                                    int wid, int nw) {
-  for (int t0 = 0; t0 < s; t0 += 16) {
-    const int t1 = min(s, t0 + 16);
-    if (wid == 0) {
-      for (int t = t0 + 1; t < t1; ++t) {
-        double v = R[t * kPanelW + lane];
-        for (int tp = t0; tp < t; ++tp) v -= Lr[t + (size_t)tp * c] * R[tp * kPanelW + lane];
-        R[t * kPanelW + lane] = v;
+// backward, big supernode r: x[S] = L_SS^{-T} (z[S] - L_US^T x[U]), chunks descending; each chunk
+// takes the rows of S after it as part of its gather (they are final by then)
+__device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, const int32_t* __restrict__ U,
+                        double* X, bool onpath, double* Vs, int tid, int lane, int wid, int nw) {
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int nch = (s + kChunk - 1) / kChunk;
+  for (int ch = nch - 1; ch >= 0; --ch) {
+    const int t0 = ch * kChunk, w = min(kChunk, s - t0), t1 = t0 + w;
+    const int ntt = (w + 7) >> 3;
+    for (int task = wid; task < ntt * 4; task += nw) {
+      const int tt = task >> 2, n0 = (task & 3) * 8;
+      const int r0 = tt * 8 + g8;
+      double c0 = 0.0, c1 = 0.0;
+      if (onpath && r0 < w) {
+        c0 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4];
+        c1 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4 + 1];
+      }
+      // A(t, k) = L[t1 + k][t0 + tt*8 + t]: as_t = c, as_k = 1; K = c - t1 (rows S_>c, then U)
+      double d0 = 0.0, d1 = 0.0;
+      tile_gemm_gather(d0, d1, Lr + t1 + (size_t)(t0 + tt * 8) * c, c, 1, min(8, w - tt * 8), X, t1, c - t1, f, s, U,
+                       n0, lane);
+      if (r0 < w) {
+        Vs[r0 * kVs + n0 + 2 * t4] = c0 - d0;
+        Vs[r0 * kVs + n0 + 2 * t4 + 1] = c1 - d1;
       }
     }
     __syncthreads();
-    for (int t = t1 + wid; t < s; t += nw) {
-      double v = R[t * kPanelW + lane];
-      for (int tp = t0; tp < t1; ++tp) v -= Lr[t + (size_t)tp * c] * R[tp * kPanelW + lane];
-      R[t * kPanelW + lane] = v;
+    // chunk triangle L_cc^T, 16-row diagonal blocks from the bottom up
+    const int nb = (w + 15) / 16;
+    for (int bb = nb - 1; bb >= 0; --bb) {
+      const int b0 = bb * 16, bw = min(16, w - b0);
+      if (wid == 0) {
+        double acc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = j < bw ? Vs[(b0 + j) * kVs + lane] : 0.0;
+#pragma unroll
+        for (int j = 15; j >= 0; --j) {
+          if (j < bw) {
+#pragma unroll
+            for (int jj = 0; jj < j; ++jj) acc[jj] -= Lr[(t0 + b0 + j) + (size_t)(t0 + b0 + jj) * c] * acc[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < bw) Vs[(b0 + j) * kVs + lane] = acc[j];
+      }
+      __syncthreads();
+      for (int t = wid; t < b0; t += nw) {
+        double v = Vs[t * kVs + lane];
+        for (int j = 0; j < bw; ++j) v -= Lr[(t0 + b0 + j) + (size_t)(t0 + t) * c] * Vs[(b0 + j) * kVs + lane];
+        Vs[t * kVs + lane] = v;
+      }
+      __syncthreads();
     }
+    for (int t = wid; t < w; t += nw) X[(size_t)(f + t0 + t) * kPanelW + lane] = Vs[t * kVs + lane];
     __syncthreads();
-  }
-}
-
-// forward U update from staged S rows: x[U_q] -= sum_t L[s+q, t] R[t], 2 rows per warp in flight
-__device__ __forceinline__ void coop_fwd_update_staged(const double* __restrict__ Lr, int c, int s,
-                                                       const int32_t* __restrict__ U, const double* R, double* X,
-                                                       int lane, int wid, int nw) {
-  const int u = c - s;
-  for (int qq = wid; qq < u; qq += 2 * nw) {
-    const int q2 = qq + nw;
-    const int r1 = U[qq], r2 = q2 < u ? U[q2] : r1;
-    double x1 = xrow(X, r1, lane), x2 = q2 < u ? xrow(X, r2, lane) : 0.0;
-    for (int t = 0; t < s; ++t) {
-      const double z = R[t * kPanelW + lane];
-      x1 -= Lr[s + qq + (size_t)t * c] * z;
-      if (q2 < u) x2 -= Lr[s + q2 + (size_t)t * c] * z;
-    }
-    xrow(X, r1, lane) = x1;
-    if (q2 < u) xrow(X, r2, lane) = x2;
   }
 }
 
@@ -219,8 +289,8 @@ __device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c,
 
 __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double smem_solve[];
-  double* R = smem_solve;                                                               // staged rows
-  uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + kStageRows * kPanelW);  // bitmap
+  double* Vs = smem_solve;                                                          // chunk of S rows
+  uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + kChunk * kVs);      // bitmap
   const int P = blockIdx.x, fac = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSolveThreads / 32;
@@ -252,12 +322,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
     const double* Lr = Lp + a.panel_off[r];
-    if (s > 16 && s <= kStageRows) {
-      // big supernode: S rows staged in shared memory, triangle and U update from there
-      stage_rows(R, X, f, s, nullptr, 0, true, tid, kSolveThreads);
-      coop_fwd_tri_staged(Lr, c, s, R, lane, wid, NW);
-      for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) = R[t * kPanelW + lane];
-      if (u > 0) coop_fwd_update_staged(Lr, c, s, rowind + a.colptr[f] + s, R, X, lane, wid, NW);
+    if (s >= kBigS) {
+      big_fwd(Lr, c, s, f, rowind + a.colptr[f] + s, X, Vs, tid, lane, wid, NW);
     } else {
       if (wid == 0) {  // unit lower diagonal block in registers, chunks of 16
         for (int t0 = 0; t0 < s; t0 += 16) {
@@ -308,14 +374,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
     const double* Lr = Lp + a.panel_off[r];
     const int32_t* U = rowind + a.colptr[f] + s;
-    if (c <= kStageRows) {
-      stage_rows(R, X, f, s, U, c - s, onpath, tid, kSolveThreads);
-      coop_bwd_staged(Lr, c, s, R, lane, wid, NW);
-      for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) = R[t * kPanelW + lane];
-    } else if (wid == 0) {  // very large clique: one warp from global memory
-      bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
-    }
-    __syncthreads();
+    big_bwd(Lr, c, s, f, U, X, onpath, Vs, tid, lane, wid, NW);
   }
   int* ctr = reinterpret_cast<int*>(inreach + nwords);
   if (tid == 0) *ctr = 0;
@@ -367,7 +426,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.D[1] = h->Dy;
   a.out[0] = h->Xh;
   a.out[1] = h->Yh;
-  size_t smem = sizeof(double) * kStageRows * kPanelW + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
+  size_t smem = sizeof(double) * kChunk * kVs + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);

@@ -1,0 +1,65 @@
+// Microbenchmark: cycles of the 32x32 warp Cholesky + inverse used by the Cholesky diagonal kernel
+// (variants: noinline generic pointers vs inline shared).  Build: nvcc -arch=sm_100a -O3.
+#include <cstdio>
+#include <cuda_runtime.h>
+constexpr int kLdD = 132;
+__device__ __forceinline__ int chol_body(double* Ab, double (*Tinv)[33], int lane) {
+  double row[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * kLdD] : 0.0;
+  int fail = -1;
+  double rinv = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, row[j], j);
+    if (fail < 0 && !(d > 0.0)) fail = j;
+    const double rl = rsqrt(d);
+    if (lane == j) { row[j] = d * rl; rinv = rl; } else if (lane > j) { row[j] *= rl; }
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, row[j], k);
+      if (lane >= k) row[k] -= row[j] * lkj;
+    }
+  }
+  if (fail >= 0) return fail;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) if (c <= lane) Ab[lane + c * kLdD] = row[c];
+  __syncwarp();
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    x[i] *= __shfl_sync(0xffffffffu, rinv, i);
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) x[k] -= Ab[k + i * kLdD] * x[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Tinv[i][lane] = i >= lane ? x[i] : 0.0;
+  return -1;
+}
+__device__ __noinline__ int chol_noinline(double* Ab, double (*Tinv)[33], int lane) { return chol_body(Ab, Tinv, lane); }
+template <int V>
+__global__ void k(const double* g, long long* cyc, double* out) {
+  __shared__ double A[32 * kLdD];
+  __shared__ double T[32][33];
+  for (int i = threadIdx.x; i < 32 * kLdD; i += blockDim.x) A[i] = g[i];
+  __syncthreads();
+  long long t0 = clock64();
+  int r = 0;
+  if (threadIdx.x < 32) r = V == 0 ? chol_noinline(A, T, threadIdx.x) : chol_body(A, T, threadIdx.x);
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) { cyc[V] = t1 - t0; out[V] = T[31][0] + r; }
+}
+int main() {
+  double h[32 * kLdD];
+  for (int i = 0; i < 32; ++i) for (int j = 0; j < 32; ++j) h[i + j * kLdD] = (i == j ? 40.0 : 0.0) + 1.0 / (1 + i + j);
+  double *g, *o; long long* c;
+  cudaMalloc(&g, sizeof h); cudaMalloc(&o, 64); cudaMalloc(&c, 64);
+  cudaMemcpy(g, h, sizeof h, cudaMemcpyHostToDevice);
+  for (int rep = 0; rep < 3; ++rep) { k<0><<<1, 256>>>(g, c, o); k<1><<<1, 256>>>(g, c, o); }
+  long long hc[2]; cudaMemcpy(hc, c, 16, cudaMemcpyDeviceToHost);
+  printf("warp_chol_inv32 cycles: noinline %lld, inline %lld\n", hc[0], hc[1]);
+  return 0;
+}
