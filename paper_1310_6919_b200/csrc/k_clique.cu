@@ -140,38 +140,29 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
         }
       }
       __syncthreads();
-      // trailing update of rows/cols >= r0: A[i,j] -= sum_k P[i,k] P[j,k], 4 x 4 register tiles
-      const int nb4 = (nr + 3) >> 2;
-      const int ntile = nb4 * (nb4 + 1) / 2;
-      for (int t = tid; t < ntile; t += NT) {
-        int bi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-        while (bi * (bi + 1) / 2 > t) --bi;
-        while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-        const int bj = t - bi * (bi + 1) / 2;
-        const int i0 = r0 + bi * 4, jj0 = r0 + bj * 4;
-        double acc[4][4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-        for (int k = 0; k < jw; ++k) {
-          double pi[4], pj[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) pi[a] = (i0 + a < c) ? P[i0 + a + (size_t)k * ld] : 0.0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b) pj[b] = (jj0 + b < c) ? P[jj0 + b + (size_t)k * ld] : 0.0;
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] += pi[a] * pj[b];
+      // trailing update of rows/cols >= r0: A[i,j] -= sum_k P[i,k] P[j,k] on the FP64 tensor cores,
+      // one 8 x 8 lower tile per warp task (m8n8k4 DMMA, K = jw), C read-modify-written in place
+      const int lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
+      const int nb8 = (nr + 7) >> 3, ntile = nb8 * (nb8 + 1) / 2;
+      for (int t = wid; t < ntile; t += NT / 32) {
+        int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while (ti * (ti + 1) / 2 > t) --ti;
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int i = r0 + ti * 8 + g8, j = r0 + tj * 8 + 2 * t4;
+        const bool iv = i < c;
+        double c0 = (iv && j < c && j <= i) ? A[i + (size_t)j * ld] : 0.0;
+        double c1 = (iv && j + 1 < c && j + 1 <= i) ? A[i + (size_t)(j + 1) * ld] : 0.0;
+        const int ia = r0 + ti * 8 + g8, ja = r0 + tj * 8 + g8;
+#pragma unroll 4
+        for (int k0 = 0; k0 < jw; k0 += 4) {
+          const int k = k0 + t4;
+          const double av = (ia < c && k < jw) ? P[ia + (size_t)k * ld] : 0.0;
+          const double bv = (ja < c && k < jw) ? P[ja + (size_t)k * ld] : 0.0;
+          dmma_8x8x4(c0, c1, -av, bv);
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int i = i0 + a, j = jj0 + b;
-            if (i < c && j < c && i >= j) A[i + (size_t)j * ld] -= acc[a][b];
-          }
+        if (iv && j < c && j <= i) A[i + (size_t)j * ld] = c0;
+        if (iv && j + 1 < c && j + 1 <= i) A[i + (size_t)(j + 1) * ld] = c1;
       }
     }
     __syncthreads();
@@ -198,14 +189,26 @@ __device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, 
     // W[J, t] -= sum_{i >= jb+jw} M[i, jb+q] W[i, t]
     const int lo = jb + jw;
     if (lo < c && ns > 0) {
-      for (int idx = tid; idx < jw * ns; idx += NT) {
-        const int q = idx % jw, t = t0 + idx / jw;
-        const double* Mc = A + (size_t)(jb + q) * c;
-        const double* Wc = W + (size_t)t * c;
-        const int hi = min(c, u + t + 1);  // W[i, t] = 0 for i > u + t
-        double acc = 0.0;
-        for (int i = lo; i < hi; ++i) acc += Mc[i] * Wc[i];
-        W[jb + q + (size_t)t * c] -= acc;
+      // DMMA 8 x 8 tiles (q block x t block), K = c - lo; rows i > u + t of W are zero, so the
+      // full K range adds nothing there
+      const int g8 = lane >> 2, t4 = lane & 3;
+      const int nq8 = (jw + 7) >> 3, nt8 = (ns + 7) >> 3, K = c - lo;
+      for (int task = wid; task < nq8 * nt8; task += NT / 32) {
+        const int qb = (task % nq8) * 8, tb = t0 + (task / nq8) * 8;
+        const int qa = qb + g8, ta = tb + g8;
+        const double* Ap = A + lo + (size_t)(jb + qa) * c;
+        const double* Bp = W + lo + (size_t)ta * c;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll 4
+        for (int k0 = 0; k0 < K; k0 += 4) {
+          const int k = k0 + t4;
+          const double av = (qa < jw && k < K) ? Ap[k] : 0.0;
+          const double bv = (ta < s && k < K) ? Bp[k] : 0.0;
+          dmma_8x8x4(c0, c1, av, bv);
+        }
+        const int q = qb + g8, t = tb + 2 * t4;
+        if (q < jw && t < s) W[jb + q + (size_t)t * c] -= c0;
+        if (q < jw && t + 1 < s) W[jb + q + (size_t)(t + 1) * c] -= c1;
       }
     }
     // inverse of the diagonal block M[J,J] (lower): warp 0

@@ -124,7 +124,7 @@ __device__ __forceinline__ void tile_gemm_gather(double& c0, double& c1, const d
   const int g8 = lane >> 2, t4 = lane & 3;
   const bool tv = g8 < nt;
   const double* ap = Ab + (size_t)g8 * as_t + (size_t)t4 * as_k;
-#pragma unroll 2
+#pragma unroll 8
   for (int k0 = 0; k0 < K; k0 += 4) {
     const int k = k0 + t4;
     const bool kv = k < K;
@@ -208,29 +208,83 @@ __device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, cons
 }
 
 // backward, big supernode r: x[S] = L_SS^{-T} (z[S] - L_US^T x[U]), chunks descending; each chunk
-// takes the rows of S after it as part of its gather (they are final by then)
+// takes the rows of S after it as part of its gather (they are final by then).  The gathered X rows
+// (the B operand, shared by every output tile of the chunk) are staged in shared memory in K-chunks
+// of kKc rows, double-buffered with cp.async; each warp keeps the accumulators of its tiles across
+// K-chunks.  The A operand (panel L_r) streams from L2 with independent loads.
+constexpr int kKc = 64;                  // gathered rows per staged K-chunk
+constexpr int kMaxTasks = kChunk / 8 * 4 / 8;  // tiles per warp (8 warps, 128-row chunk, 4 RHS slices)
+
+__device__ __forceinline__ void stage_gather(double* Bsb, const double* X, int kb0, int nrows, int f, int s,
+                                             const int32_t* __restrict__ U, int tid, int nt) {
+  for (int idx = tid; idx < kKc * 16; idx += nt) {  // 16 x 16-byte pieces per 256-byte row
+    const int rr = idx >> 4, ch = idx & 15;
+    const bool v = rr < nrows;
+    const int row = v ? op_row(kb0 + rr, f, s, U) : 0;
+    cp_async16(Bsb + rr * kVs + ch * 2, X + (size_t)row * kPanelW + ch * 2, v);
+  }
+  cp_async_commit();
+}
+
 __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, const int32_t* __restrict__ U,
-                        double* X, bool onpath, double* Vs, int tid, int lane, int wid, int nw) {
+                        double* X, bool onpath, double* Vs, double* Bs, int tid, int lane, int wid, int nw) {
   const int g8 = lane >> 2, t4 = lane & 3;
   const int nch = (s + kChunk - 1) / kChunk;
   for (int ch = nch - 1; ch >= 0; --ch) {
     const int t0 = ch * kChunk, w = min(kChunk, s - t0), t1 = t0 + w;
-    const int ntt = (w + 7) >> 3;
-    for (int task = wid; task < ntt * 4; task += nw) {
-      const int tt = task >> 2, n0 = (task & 3) * 8;
-      const int r0 = tt * 8 + g8;
-      double c0 = 0.0, c1 = 0.0;
-      if (onpath && r0 < w) {
-        c0 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4];
-        c1 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4 + 1];
+    const int ntt = (w + 7) >> 3, ntask = ntt * 4;
+    const int K = c - t1;  // gathered rows: S after the chunk, then U
+    double acc[kMaxTasks][2];
+#pragma unroll
+    for (int q = 0; q < kMaxTasks; ++q) acc[q][0] = acc[q][1] = 0.0;
+    const int nkc = (K + kKc - 1) / kKc;
+    if (nkc > 0) stage_gather(Bs, X, t1, min(kKc, K), f, s, U, tid, nw * 32);
+    for (int kc = 0; kc < nkc; ++kc) {
+      const double* Bb = Bs + (kc & 1) * kKc * kVs;
+      if (kc + 1 < nkc) {
+        stage_gather(Bs + ((kc + 1) & 1) * kKc * kVs, X, t1 + (kc + 1) * kKc, min(kKc, K - (kc + 1) * kKc), f, s,
+                     U, tid, nw * 32);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
-      // A(t, k) = L[t1 + k][t0 + tt*8 + t]: as_t = c, as_k = 1; K = c - t1 (rows S_>c, then U)
-      double d0 = 0.0, d1 = 0.0;
-      tile_gemm_gather(d0, d1, Lr + t1 + (size_t)(t0 + tt * 8) * c, c, 1, min(8, w - tt * 8), X, t1, c - t1, f, s, U,
-                       n0, lane);
-      if (r0 < w) {
-        Vs[r0 * kVs + n0 + 2 * t4] = c0 - d0;
-        Vs[r0 * kVs + n0 + 2 * t4 + 1] = c1 - d1;
+      __syncthreads();
+      const int kr = min(kKc, K - kc * kKc);
+#pragma unroll
+      for (int q = 0; q < kMaxTasks; ++q) {
+        const int task = wid + q * nw;
+        if (task < ntask) {
+          const int tt = task >> 2, n0 = (task & 3) * 8;
+          const bool tv = tt * 8 + g8 < w;
+          // A(t, k) = L[t1 + kc*kKc + k][t0 + tt*8 + t]
+          const double* ap = Lr + t1 + kc * kKc + t4 + (size_t)(t0 + tt * 8 + g8) * c;
+          const double* bp = Bb + t4 * kVs + n0 + g8;
+#pragma unroll 8
+          for (int k0 = 0; k0 < kKc; k0 += 4) {
+            const bool kv = k0 + t4 < kr;
+            const double av = (tv && kv) ? ap[k0] : 0.0;
+            const double bv = kv ? bp[k0 * kVs] : 0.0;
+            dmma_8x8x4(acc[q][0], acc[q][1], av, bv);
+          }
+        }
+      }
+      __syncthreads();  // buffer (kc & 1) is refilled by the next iteration's prefetch
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxTasks; ++q) {
+      const int task = wid + q * nw;
+      if (task < ntask) {
+        const int tt = task >> 2, n0 = (task & 3) * 8;
+        const int r0 = tt * 8 + g8;
+        if (r0 < w) {
+          double z0 = 0.0, z1 = 0.0;
+          if (onpath) {
+            z0 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4];
+            z1 = X[(size_t)(f + t0 + r0) * kPanelW + n0 + 2 * t4 + 1];
+          }
+          Vs[r0 * kVs + n0 + 2 * t4] = z0 - acc[q][0];
+          Vs[r0 * kVs + n0 + 2 * t4 + 1] = z1 - acc[q][1];
+        }
       }
     }
     __syncthreads();
@@ -239,19 +293,19 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
     for (int bb = nb - 1; bb >= 0; --bb) {
       const int b0 = bb * 16, bw = min(16, w - b0);
       if (wid == 0) {
-        double acc[16];
+        double acc16[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = j < bw ? Vs[(b0 + j) * kVs + lane] : 0.0;
+        for (int j = 0; j < 16; ++j) acc16[j] = j < bw ? Vs[(b0 + j) * kVs + lane] : 0.0;
 #pragma unroll
         for (int j = 15; j >= 0; --j) {
           if (j < bw) {
 #pragma unroll
-            for (int jj = 0; jj < j; ++jj) acc[jj] -= Lr[(t0 + b0 + j) + (size_t)(t0 + b0 + jj) * c] * acc[j];
+            for (int jj = 0; jj < j; ++jj) acc16[jj] -= Lr[(t0 + b0 + j) + (size_t)(t0 + b0 + jj) * c] * acc16[j];
           }
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (j < bw) Vs[(b0 + j) * kVs + lane] = acc[j];
+          if (j < bw) Vs[(b0 + j) * kVs + lane] = acc16[j];
       }
       __syncthreads();
       for (int t = wid; t < b0; t += nw) {
@@ -290,7 +344,8 @@ __device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c,
 __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double smem_solve[];
   double* Vs = smem_solve;                                                          // chunk of S rows
-  uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + kChunk * kVs);      // bitmap
+  double* Bs = smem_solve + kChunk * kVs;                                           // 2 staged K-chunks
+  uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + (kChunk + 2 * kKc) * kVs);  // bitmap
   const int P = blockIdx.x, fac = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSolveThreads / 32;
@@ -374,7 +429,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
     const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
     const double* Lr = Lp + a.panel_off[r];
     const int32_t* U = rowind + a.colptr[f] + s;
-    big_bwd(Lr, c, s, f, U, X, onpath, Vs, tid, lane, wid, NW);
+    big_bwd(Lr, c, s, f, U, X, onpath, Vs, Bs, tid, lane, wid, NW);
   }
   int* ctr = reinterpret_cast<int*>(inreach + nwords);
   if (tid == 0) *ctr = 0;
@@ -426,7 +481,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.D[1] = h->Dy;
   a.out[0] = h->Xh;
   a.out[1] = h->Yh;
-  size_t smem = sizeof(double) * kChunk * kVs + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
+  size_t smem = sizeof(double) * (kChunk + 2 * kKc) * kVs + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
