@@ -45,7 +45,6 @@ struct SolveArgs {
 };
 
 constexpr int kSolveThreads = 256;
-constexpr int kCh = 16;  // register chunk of supernode columns (widest instantiation)
 
 __device__ __forceinline__ double& xrow(double* X, int row, int lane) { return X[(size_t)row * kPanelW + lane]; }
 
@@ -320,24 +319,33 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
   }
 }
 
-// forward update of the U rows of one supernode by all warps: x[U] -= L_US z[S] (S rows final)
+// forward for a small supernode (s < kBigS), no barrier inside: every warp solves the unit-lower
+// L_SS block for the 32 RHS in registers (redundantly: s <= 15), warp 0 writes z[S] back, and each
+// warp then updates its share of the rows U with the register copy of z[S]
 template <int kCh>
-__device__ __forceinline__ void fwd_update(const double* __restrict__ Lr, int c, int s, int f,
-                                           const int32_t* __restrict__ U, double* X, int lane, int wid, int nw) {
+__device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, int s, int f,
+                                          const int32_t* __restrict__ U, double* X, int lane, int wid, int nw) {
+  double zt[kCh];
+#pragma unroll
+  for (int j = 0; j < kCh; ++j) zt[j] = j < s ? xrow(X, f + j, lane) : 0.0;
+#pragma unroll
+  for (int j = 0; j < kCh; ++j)
+#pragma unroll
+    for (int jj = j + 1; jj < kCh; ++jj)
+      if (jj < s) zt[jj] -= Lr[jj + (size_t)j * c] * zt[j];
+  if (wid == 0) {
+#pragma unroll
+    for (int j = 0; j < kCh; ++j)
+      if (j < s) xrow(X, f + j, lane) = zt[j];
+  }
   const int u = c - s;
-  for (int t0 = 0; t0 < s; t0 += kCh) {
-    const int w = min(kCh, s - t0);
-    double zt[kCh];
+  for (int qq = wid; qq < u; qq += nw) {
+    const int row = U[qq];
+    double acc = xrow(X, row, lane);
 #pragma unroll
-    for (int j = 0; j < kCh; ++j) zt[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
-    const double* Lc = Lr + (size_t)t0 * c;
-    for (int qq = wid; qq < u; qq += nw) {
-      double acc = xrow(X, U[qq], lane);
-#pragma unroll
-      for (int j = 0; j < kCh; ++j)
-        if (j < w) acc -= Lc[s + qq + (size_t)j * c] * zt[j];
-      xrow(X, U[qq], lane) = acc;
-    }
+    for (int j = 0; j < kCh; ++j)
+      if (j < s) acc -= Lr[s + qq + (size_t)j * c] * zt[j];
+    xrow(X, row, lane) = acc;
   }
 }
 
@@ -375,47 +383,25 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   // forward L z = E_P over the paths, ascending supernodes
   for (int q = rb; q < re; ++q) {
     const int r = a.reach_sn[q];
-    const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
+    const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
     const double* Lr = Lp + a.panel_off[r];
     if (s >= kBigS) {
       big_fwd(Lr, c, s, f, rowind + a.colptr[f] + s, X, Vs, tid, lane, wid, NW);
     } else {
-      if (wid == 0) {  // unit lower diagonal block in registers, chunks of 16
-        for (int t0 = 0; t0 < s; t0 += 16) {
-          const int w = min(16, s - t0);
-          double acc[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] = j < w ? xrow(X, f + t0 + j, lane) : 0.0;
-          for (int tp = 0; tp < t0; ++tp) {
-            const double zt = xrow(X, f + tp, lane);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < w) acc[j] -= Lr[(t0 + j) + (size_t)tp * c] * zt;
-          }
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j < w) {
-              const double zj = acc[j];
-              xrow(X, f + t0 + j, lane) = zj;
-#pragma unroll
-              for (int jj = j + 1; jj < 16; ++jj)
-                if (jj < w) acc[jj] -= Lr[(t0 + jj) + (size_t)(t0 + j) * c] * zj;
-            }
-          }
-        }
-      }
-      __syncthreads();
-      if (u > 0) {
-        const int32_t* U = rowind + a.colptr[f] + s;
-        if (s <= 1) fwd_update<1>(Lr, c, s, f, U, X, lane, wid, NW);
-        else if (s <= 2) fwd_update<2>(Lr, c, s, f, U, X, lane, wid, NW);
-        else if (s <= 4) fwd_update<4>(Lr, c, s, f, U, X, lane, wid, NW);
-        else if (s <= 8) fwd_update<8>(Lr, c, s, f, U, X, lane, wid, NW);
-        else fwd_update<16>(Lr, c, s, f, U, X, lane, wid, NW);
-      }
+      const int32_t* U = rowind + a.colptr[f] + s;
+      if (s <= 1) fwd_small<1>(Lr, c, s, f, U, X, lane, wid, NW);
+      else if (s <= 2) fwd_small<2>(Lr, c, s, f, U, X, lane, wid, NW);
+      else if (s <= 4) fwd_small<4>(Lr, c, s, f, U, X, lane, wid, NW);
+      else if (s <= 8) fwd_small<8>(Lr, c, s, f, U, X, lane, wid, NW);
+      else fwd_small<16>(Lr, c, s, f, U, X, lane, wid, NW);
     }
     __syncthreads();
-    for (int t = wid; t < s; t += NW) xrow(X, f + t, lane) /= D[f + t];
+  }
+  // z <- D^{-1} z on the path rows (deferred: the U updates above use the unscaled z)
+  for (int q = rb + wid; q < re; q += NW) {
+    const int r = a.reach_sn[q];
+    const int f = a.super_ptr[r], s = a.sns[r];
+    for (int t = 0; t < s; ++t) xrow(X, f + t, lane) /= D[f + t];
   }
   __syncthreads();
 

@@ -39,6 +39,42 @@ __device__ __forceinline__ int chol_body(double* Ab, double (*Tinv)[33], int lan
   return -1;
 }
 __device__ __noinline__ int chol_noinline(double* Ab, double (*Tinv)[33], int lane) { return chol_body(Ab, Tinv, lane); }
+// factor only (no inverse)
+__device__ __forceinline__ int factor_only(double* Ab, int lane) {
+  double row[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * kLdD] : 0.0;
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = __shfl_sync(0xffffffffu, row[j], j);
+    if (fail < 0 && !(d > 0.0)) fail = j;
+    const double rl = rsqrt(d);
+    if (lane == j) row[j] = d * rl; else if (lane > j) row[j] *= rl;
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, row[j], k);
+      if (lane >= k) row[k] -= row[j] * lkj;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) if (c <= lane) Ab[lane + c * kLdD] = row[c];
+  return fail;
+}
+// inverse only (L given in Ab, unit diag scaling by 1/L_ii from smem)
+__device__ __forceinline__ void inverse_only(const double* Ab, double (*Tinv)[33], int lane) {
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    x[i] *= 1.0 / Ab[i + i * kLdD];
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) x[k] -= Ab[k + i * kLdD] * x[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Tinv[i][lane] = i >= lane ? x[i] : 0.0;
+}
 template <int V>
 __global__ void k(const double* g, long long* cyc, double* out) {
   __shared__ double A[32 * kLdD];
@@ -47,7 +83,12 @@ __global__ void k(const double* g, long long* cyc, double* out) {
   __syncthreads();
   long long t0 = clock64();
   int r = 0;
-  if (threadIdx.x < 32) r = V == 0 ? chol_noinline(A, T, threadIdx.x) : chol_body(A, T, threadIdx.x);
+  if (threadIdx.x < 32) {
+    if (V == 0) r = chol_noinline(A, T, threadIdx.x);
+    else if (V == 1) r = chol_body(A, T, threadIdx.x);
+    else if (V == 2) r = factor_only(A, threadIdx.x);
+    else inverse_only(A, T, threadIdx.x);
+  }
   __syncthreads();
   long long t1 = clock64();
   if (threadIdx.x == 0) { cyc[V] = t1 - t0; out[V] = T[31][0] + r; }
@@ -58,8 +99,8 @@ int main() {
   double *g, *o; long long* c;
   cudaMalloc(&g, sizeof h); cudaMalloc(&o, 64); cudaMalloc(&c, 64);
   cudaMemcpy(g, h, sizeof h, cudaMemcpyHostToDevice);
-  for (int rep = 0; rep < 3; ++rep) { k<0><<<1, 256>>>(g, c, o); k<1><<<1, 256>>>(g, c, o); }
-  long long hc[2]; cudaMemcpy(hc, c, 16, cudaMemcpyDeviceToHost);
-  printf("warp_chol_inv32 cycles: noinline %lld, inline %lld\n", hc[0], hc[1]);
+  for (int rep = 0; rep < 3; ++rep) { k<0><<<1, 256>>>(g, c, o); k<1><<<1, 256>>>(g, c, o); k<2><<<1, 256>>>(g, c, o); k<3><<<1, 256>>>(g, c, o); }
+  long long hc[4]; cudaMemcpy(hc, c, 32, cudaMemcpyDeviceToHost);
+  printf("warp_chol_inv32 cycles: noinline %lld, inline %lld, factor only %lld, inverse only %lld\n", hc[0], hc[1], hc[2], hc[3]);
   return 0;
 }
