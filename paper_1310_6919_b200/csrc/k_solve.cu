@@ -320,11 +320,13 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
 }
 
 // forward for a small supernode (s < kBigS), no barrier inside: every warp solves the unit-lower
-// L_SS block for the 32 RHS in registers (redundantly: s <= 15), warp 0 writes z[S] back, and each
-// warp then updates its share of the rows U with the register copy of z[S]
+// L_SS block for the 32 RHS in registers (redundantly: s <= 15) and updates its share of the rows U
+// with that copy of z[S]; warp 0 parks z[S] in a shared-memory slot (zslot[j*32 + lane]), copied to
+// X after the next barrier (writing X[S] here could race with a slower warp still reading it)
 template <int kCh>
 __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, int s, int f,
-                                          const int32_t* __restrict__ U, double* X, int lane, int wid, int nw) {
+                                          const int32_t* __restrict__ U, double* X, double* zslot, int lane,
+                                          int wid, int nw) {
   double zt[kCh];
 #pragma unroll
   for (int j = 0; j < kCh; ++j) zt[j] = j < s ? xrow(X, f + j, lane) : 0.0;
@@ -336,7 +338,7 @@ __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, 
   if (wid == 0) {
 #pragma unroll
     for (int j = 0; j < kCh; ++j)
-      if (j < s) xrow(X, f + j, lane) = zt[j];
+      if (j < s) zslot[j * kPanelW + lane] = zt[j];
   }
   const int u = c - s;
   for (int qq = wid; qq < u; qq += nw) {
@@ -380,23 +382,40 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   }
   __syncthreads();
 
-  // forward L z = E_P over the paths, ascending supernodes
+  // forward L z = E_P over the paths, ascending supernodes.  Small supernodes park their z[S] in
+  // one of two shared-memory slots (Bs is free during the forward), flushed after the next barrier.
+  double* zslots = Bs;
+  int pend_f = -1, pend_s = 0, pend_slot = 0, slot = 0;
+  auto flush = [&](int wflush) {
+    if (pend_f >= 0 && wid == wflush)
+      for (int t = 0; t < pend_s; ++t) xrow(X, pend_f + t, lane) = zslots[(pend_slot * 16 + t) * kPanelW + lane];
+    pend_f = -1;
+  };
   for (int q = rb; q < re; ++q) {
     const int r = a.reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
     const double* Lr = Lp + a.panel_off[r];
+    flush(NW - 1);
     if (s >= kBigS) {
+      __syncthreads();
       big_fwd(Lr, c, s, f, rowind + a.colptr[f] + s, X, Vs, tid, lane, wid, NW);
     } else {
       const int32_t* U = rowind + a.colptr[f] + s;
-      if (s <= 1) fwd_small<1>(Lr, c, s, f, U, X, lane, wid, NW);
-      else if (s <= 2) fwd_small<2>(Lr, c, s, f, U, X, lane, wid, NW);
-      else if (s <= 4) fwd_small<4>(Lr, c, s, f, U, X, lane, wid, NW);
-      else if (s <= 8) fwd_small<8>(Lr, c, s, f, U, X, lane, wid, NW);
-      else fwd_small<16>(Lr, c, s, f, U, X, lane, wid, NW);
+      double* zs = zslots + slot * 16 * kPanelW;
+      if (s <= 1) fwd_small<1>(Lr, c, s, f, U, X, zs, lane, wid, NW);
+      else if (s <= 2) fwd_small<2>(Lr, c, s, f, U, X, zs, lane, wid, NW);
+      else if (s <= 4) fwd_small<4>(Lr, c, s, f, U, X, zs, lane, wid, NW);
+      else if (s <= 8) fwd_small<8>(Lr, c, s, f, U, X, zs, lane, wid, NW);
+      else fwd_small<16>(Lr, c, s, f, U, X, zs, lane, wid, NW);
+      pend_f = f;
+      pend_s = s;
+      pend_slot = slot;
+      slot ^= 1;
     }
     __syncthreads();
   }
+  flush(NW - 1);
+  __syncthreads();
   // z <- D^{-1} z on the path rows (deferred: the U updates above use the unscaled z)
   for (int q = rb + wid; q < re; q += NW) {
     const int r = a.reach_sn[q];
