@@ -56,53 +56,68 @@ struct Scratch {
 };
 
 // Warp 0: Cholesky of the jw x jw block at A[j0, j0] in registers (lane = row), write it back,
-// then invert it (lane = column) into s.inv (lower, zero-padded to 32 x 32).  Returns via *flag
-// the failing local column (>= 0) or -1.
-__device__ __forceinline__ void warp_chol_inv32(double* A, int ld, int j0, int jw, const Scratch& s) {
+// then invert it (lane = column) into s.inv (lower).  NC >= jw is the unrolled block width (a
+// power of two, identity-padded beyond jw), so a 1- or 2-column supernode does not pay for 32.
+// Returns via *flag the failing local column (>= 0) or -1.  Every shuffle is executed by all lanes.
+template <int NC>
+__device__ __forceinline__ void warp_chol_inv(double* A, int ld, int j0, int jw, const Scratch& s) {
   const int lane = threadIdx.x & 31;
-  double row[32];
+  double row[NC];
 #pragma unroll
-  for (int c = 0; c < 32; ++c)
+  for (int c = 0; c < NC; ++c)
     row[c] = (lane < jw && c < jw) ? A[(j0 + lane) + (size_t)(j0 + c) * ld] : (lane == c ? 1.0 : 0.0);
   int fail = -1;
+  double rinv = 0.0;  // lane j: 1 / L[j][j]
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < NC; ++j) {
     const double d = __shfl_sync(kFullMask, row[j], j);
-    if (fail < 0) {
-      if (!(d > 0.0)) {
-        fail = j;
-      } else {
-        const double l = sqrt(d);
-        if (lane == j) row[j] = l;
-        else if (lane > j) row[j] /= l;
+    if (fail < 0 && !(d > 0.0)) fail = j;
+    const double rl = rsqrt(d);
+    if (lane == j) {
+      row[j] = d * rl;
+      rinv = rl;
+    } else if (lane > j) {
+      row[j] *= rl;
+    }
 #pragma unroll
-        for (int k = j + 1; k < 32; ++k) {
-          const double akj = __shfl_sync(kFullMask, row[j], k);
-          if (lane >= k) row[k] -= row[j] * akj;
-        }
-      }
+    for (int k = j + 1; k < NC; ++k) {
+      const double akj = __shfl_sync(kFullMask, row[j], k);
+      if (lane >= k) row[k] -= row[j] * akj;
     }
   }
+  if (fail >= jw) fail = -1;  // padding never fails; a NaN/negative pivot inside the block does
   if (lane == 0) *s.flag = fail;
   if (fail >= 0) return;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const double v = lane >= c ? row[c] : 0.0;
-    s.l11[lane + c * kLdInv] = v;
+  for (int c = 0; c < NC; ++c) {
+    const double v = (lane < NC && lane >= c) ? row[c] : 0.0;
+    if (lane < NC) s.l11[lane + c * kLdInv] = v;
     if (lane < jw && c < jw) A[(j0 + lane) + (size_t)(j0 + c) * ld] = v;
   }
   __syncwarp();
-  // inverse: x = column `lane` of L11^{-1} by forward substitution (L11 broadcast from smem)
-  double x[32];
+  // inverse, lane = column: right-looking forward substitution (independent updates per step)
+  double x[NC];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double sacc = (i == lane) ? 1.0 : 0.0;
+  for (int i = 0; i < NC; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) sacc -= s.l11[i + k * kLdInv] * x[k];
-    x[i] = sacc / s.l11[i + i * kLdInv];
+  for (int i = 0; i < NC; ++i) {
+    x[i] *= __shfl_sync(kFullMask, rinv, i);
+#pragma unroll
+    for (int k = i + 1; k < NC; ++k) x[k] -= s.l11[k + i * kLdInv] * x[i];
   }
+  if (lane < NC) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) s.inv[i + lane * kLdInv] = i >= lane ? x[i] : 0.0;
+    for (int i = 0; i < NC; ++i) s.inv[i + lane * kLdInv] = i >= lane ? x[i] : 0.0;
+  }
+}
+
+__device__ __forceinline__ void warp_chol_inv32(double* A, int ld, int j0, int jw, const Scratch& s) {
+  if (jw <= 1) warp_chol_inv<1>(A, ld, j0, jw, s);
+  else if (jw <= 2) warp_chol_inv<2>(A, ld, j0, jw, s);
+  else if (jw <= 4) warp_chol_inv<4>(A, ld, j0, jw, s);
+  else if (jw <= 8) warp_chol_inv<8>(A, ld, j0, jw, s);
+  else if (jw <= 16) warp_chol_inv<16>(A, ld, j0, jw, s);
+  else warp_chol_inv<32>(A, ld, j0, jw, s);
 }
 
 // CTA-cooperative blocked Cholesky of the leading `ncols` columns of the symmetric c x c matrix A
