@@ -71,21 +71,25 @@ __device__ __forceinline__ void warp_chol_inv(double* A, int ld, int j0, int jw,
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     const double d = __shfl_sync(kFullMask, row[j], j);
-    if (fail < 0 && !(d > 0.0)) fail = j;
-    const double rl = rsqrt(d);
-    if (lane == j) {
-      row[j] = d * rl;
-      rinv = rl;
-    } else if (lane > j) {
-      row[j] *= rl;
-    }
+    if (fail < 0) {  // uniform (d is a broadcast)
+      if (!(d > 0.0)) {
+        fail = j;
+      } else {
+        const double rl = rsqrt_nr(d);
+        if (lane == j) {
+          row[j] = d * rl;
+          rinv = rl;
+        } else if (lane > j) {
+          row[j] *= rl;
+        }
 #pragma unroll
-    for (int k = j + 1; k < NC; ++k) {
-      const double akj = __shfl_sync(kFullMask, row[j], k);
-      if (lane >= k) row[k] -= row[j] * akj;
+        for (int k = j + 1; k < NC; ++k) {
+          const double akj = __shfl_sync(kFullMask, row[j], k);
+          if (lane >= k) row[k] -= row[j] * akj;
+        }
+      }
     }
   }
-  if (fail >= jw) fail = -1;  // padding never fails; a NaN/negative pivot inside the block does
   if (lane == 0) *s.flag = fail;
   if (fail >= 0) return;
 #pragma unroll
@@ -95,15 +99,14 @@ __device__ __forceinline__ void warp_chol_inv(double* A, int ld, int j0, int jw,
     if (lane < jw && c < jw) A[(j0 + lane) + (size_t)(j0 + c) * ld] = v;
   }
   __syncwarp();
-  // inverse, lane = column: right-looking forward substitution (independent updates per step)
+  // inverse, lane = column: forward substitution, L11 broadcast from shared memory
   double x[NC];
 #pragma unroll
-  for (int i = 0; i < NC; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
   for (int i = 0; i < NC; ++i) {
-    x[i] *= __shfl_sync(kFullMask, rinv, i);
+    double sacc = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
-    for (int k = i + 1; k < NC; ++k) x[k] -= s.l11[k + i * kLdInv] * x[i];
+    for (int k = 0; k < i; ++k) sacc -= s.l11[i + k * kLdInv] * x[k];
+    x[i] = sacc * __shfl_sync(kFullMask, rinv, i);
   }
   if (lane < NC) {
 #pragma unroll
@@ -112,10 +115,7 @@ __device__ __forceinline__ void warp_chol_inv(double* A, int ld, int j0, int jw,
 }
 
 __device__ __forceinline__ void warp_chol_inv32(double* A, int ld, int j0, int jw, const Scratch& s) {
-  if (jw <= 1) warp_chol_inv<1>(A, ld, j0, jw, s);
-  else if (jw <= 2) warp_chol_inv<2>(A, ld, j0, jw, s);
-  else if (jw <= 4) warp_chol_inv<4>(A, ld, j0, jw, s);
-  else if (jw <= 8) warp_chol_inv<8>(A, ld, j0, jw, s);
+  if (jw <= 4) warp_chol_inv<4>(A, ld, j0, jw, s);
   else if (jw <= 16) warp_chol_inv<16>(A, ld, j0, jw, s);
   else warp_chol_inv<32>(A, ld, j0, jw, s);
 }

@@ -54,7 +54,7 @@ __device__ __noinline__ int warp_chol_inv32(double* Ab, double (*Tinv)[33], int 
   for (int j = 0; j < 32; ++j) {
     const double d = __shfl_sync(0xffffffffu, row[j], j);
     if (fail < 0 && !(d > 0.0)) fail = j;
-    const double rl = rsqrt(d);  // one MUFU-seeded op instead of sqrt + divide on the serial chain
+    const double rl = rsqrt_nr(d);  // one MUFU-seeded op instead of sqrt + divide on the serial chain
     if (lane == j) {
       row[j] = d * rl;
       rinv = rl;

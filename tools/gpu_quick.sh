@@ -8,3 +8,12 @@ timeout 1500 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/pyt
 timeout 400 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err; echo bench $?
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv \
    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-measure-peak > gpurun_out/ncu_launch.log 2>&1; echo ncu1 $?
+if [ -n "$NCU_KERNELS" ]; then
+  i=0
+  for k in $NCU_KERNELS; do
+    i=$((i+1))
+    timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k "regex:$k" --launch-skip 5 --launch-count 1 -o gpurun_out/prof_$i -f \
+      python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-measure-peak > gpurun_out/ncu_$i.log 2>&1; echo ncu_k$i $?
+  done
+fi

@@ -3,6 +3,13 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 constexpr int kLdD = 132;
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = y * (1.5 - 0.5 * d * y * y);
+  y = y * (1.5 - 0.5 * d * y * y);
+  return y;
+}
 __device__ __forceinline__ int chol_body(double* Ab, double (*Tinv)[33], int lane) {
   double row[32];
 #pragma unroll
@@ -13,7 +20,7 @@ __device__ __forceinline__ int chol_body(double* Ab, double (*Tinv)[33], int lan
   for (int j = 0; j < 32; ++j) {
     const double d = __shfl_sync(0xffffffffu, row[j], j);
     if (fail < 0 && !(d > 0.0)) fail = j;
-    const double rl = rsqrt(d);
+    const double rl = rsqrt_nr(d);
     if (lane == j) { row[j] = d * rl; rinv = rl; } else if (lane > j) { row[j] *= rl; }
 #pragma unroll
     for (int k = j + 1; k < 32; ++k) {
@@ -49,7 +56,7 @@ __device__ __forceinline__ int factor_only(double* Ab, int lane) {
   for (int j = 0; j < 32; ++j) {
     const double d = __shfl_sync(0xffffffffu, row[j], j);
     if (fail < 0 && !(d > 0.0)) fail = j;
-    const double rl = rsqrt(d);
+    const double rl = rsqrt_nr(d);
     if (lane == j) row[j] = d * rl; else if (lane > j) row[j] *= rl;
 #pragma unroll
     for (int k = j + 1; k < 32; ++k) {
