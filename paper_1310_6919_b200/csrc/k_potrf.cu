@@ -26,8 +26,8 @@ namespace sdpc {
 constexpr int kNB = 128;         // panel width
 constexpr int kTile = 128;        // GEMM tile rows (BM); also the row/column unit of the tile grids
 constexpr int kBN = 64;           // GEMM tile columns
-constexpr int kBK = 16;           // k-chunk per pipeline stage
-constexpr int kStages = 4;
+constexpr int kBK = 32;           // k-chunk per pipeline stage (8 DMMA k-steps per barrier)
+constexpr int kStages = 2;
 constexpr int kLdA = kTile + 4;   // smem row strides (doubles): conflict-free fragment loads
 constexpr int kLdB = kBN + 4;
 constexpr int kGemmThreads = 256;  // 8 warps x (32 x 32), 2 CTAs per SM
