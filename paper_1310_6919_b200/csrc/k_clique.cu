@@ -342,9 +342,12 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
     const int uc = a.snc[ch] - a.sns[ch];
     const int32_t* rel = a.relind + a.relind_off[ch];
     const double* Uc = a.upd + a.upd_off[ch];
-    for (int idx = tid; idx < uc * uc; idx += NT) {
-      const int ia = idx % uc, ib = idx / uc;
-      if (ia >= ib) F[rel[ia] + (size_t)rel[ib] * c] += Uc[idx];
+    // lower triangle only, one warp per column ib (coalesced U_c column, relative indices)
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int ib = wid; ib < uc; ib += NT / 32) {
+      double* Fc = F + (size_t)rel[ib] * c;
+      const double* Ucol = Uc + (size_t)ib * uc;
+      for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
     }
     __syncthreads();
   }

@@ -351,7 +351,7 @@ __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, 
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double smem_solve[];
   double* Vs = smem_solve;                                                          // chunk of S rows
   double* Bs = smem_solve + kChunk * kVs;                                           // 2 staged K-chunks

@@ -68,6 +68,32 @@ __device__ __forceinline__ int factor_only(double* Ab, int lane) {
   for (int c = 0; c < 32; ++c) if (c <= lane) Ab[lane + c * kLdD] = row[c];
   return fail;
 }
+// factor with the scaled column broadcast through shared memory (no shuffles)
+__device__ __forceinline__ int factor_lds(double* Ab, double* colbuf, int lane) {
+  double row[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * kLdD] : 0.0;
+  int fail = -1;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    // lane j: pivot; everyone needs rl = 1/sqrt(d)
+    if (lane == j) colbuf[32] = rsqrt_nr(row[j]);
+    __syncwarp();
+    const double rl = colbuf[32];
+    const double lj = row[j] * rl;  // L[lane][j] for lane > j
+    if (lane == j) row[j] = row[j] * rl;
+    else if (lane > j) row[j] = lj;
+    colbuf[lane] = lj;
+    __syncwarp();
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k)
+      if (lane >= k) row[k] -= lj * colbuf[k];
+    __syncwarp();
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) if (c <= lane) Ab[lane + c * kLdD] = row[c];
+  return fail;
+}
 // inverse only (L given in Ab, unit diag scaling by 1/L_ii from smem)
 __device__ __forceinline__ void inverse_only(const double* Ab, double (*Tinv)[33], int lane) {
   double x[32];
@@ -94,6 +120,7 @@ __global__ void k(const double* g, long long* cyc, double* out) {
     if (V == 0) r = chol_noinline(A, T, threadIdx.x);
     else if (V == 1) r = chol_body(A, T, threadIdx.x);
     else if (V == 2) r = factor_only(A, threadIdx.x);
+    else if (V == 4) r = factor_lds(A, &T[0][0], threadIdx.x);
     else inverse_only(A, T, threadIdx.x);
   }
   __syncthreads();
@@ -106,8 +133,8 @@ int main() {
   double *g, *o; long long* c;
   cudaMalloc(&g, sizeof h); cudaMalloc(&o, 64); cudaMalloc(&c, 64);
   cudaMemcpy(g, h, sizeof h, cudaMemcpyHostToDevice);
-  for (int rep = 0; rep < 3; ++rep) { k<0><<<1, 256>>>(g, c, o); k<1><<<1, 256>>>(g, c, o); k<2><<<1, 256>>>(g, c, o); k<3><<<1, 256>>>(g, c, o); }
-  long long hc[4]; cudaMemcpy(hc, c, 32, cudaMemcpyDeviceToHost);
-  printf("warp_chol_inv32 cycles: noinline %lld, inline %lld, factor only %lld, inverse only %lld\n", hc[0], hc[1], hc[2], hc[3]);
+  for (int rep = 0; rep < 3; ++rep) { k<0><<<1, 256>>>(g, c, o); k<1><<<1, 256>>>(g, c, o); k<2><<<1, 256>>>(g, c, o); k<3><<<1, 256>>>(g, c, o); k<4><<<1, 256>>>(g, c, o); }
+  long long hc[5]; cudaMemcpy(hc, c, 40, cudaMemcpyDeviceToHost);
+  printf("warp_chol_inv32 cycles: noinline %lld, inline %lld, factor only %lld, inverse only %lld, factor lds %lld\n", hc[0], hc[1], hc[2], hc[3], hc[4]);
   return 0;
 }
