@@ -136,8 +136,16 @@ sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t 
 sdpc_status sdpc_get_y_factor(sdpc_handle h, double* LY_E, double* DY, void* stream);
 
 /*
+ * Truncated backward sweep (default on).  For a max-cut SCM on one rank (B = X-hat o Y^{-1}),
+ * the multi-RHS backward solve for the RHS panel starting at column p stops at row p: the entry
+ * {k, l} of B is taken from the panel of the smaller elimination index (SURVEY §8(a) notes).
+ * Off (0): every column is solved in full (needed for sdpc_get_inverse_columns).
+ */
+sdpc_status sdpc_set_truncation(sdpc_handle h, int32_t on);
+
+/*
  * Copy selected columns of X-hat and Y^{-1} computed by the last sdpc_scm_build ((b) output,
- * for verification).  cols: HOST [ncols] ORIGINAL vertex ids.  X_out, Y_out: DEVICE
+ * for verification; STATE if that build used the truncated sweep).  cols: HOST [ncols] ORIGINAL vertex ids.  X_out, Y_out: DEVICE
  * n x ncols column-major (ld = n), rows in ORIGINAL order.
  */
 sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t ncols,

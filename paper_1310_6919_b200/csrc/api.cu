@@ -422,6 +422,12 @@ sdpc_status sdpc_get_scm_layout(sdpc_handle h, sdpc_layout* out) {
   return SDPC_OK;
 }
 
+sdpc_status sdpc_set_truncation(sdpc_handle h, int32_t on) {
+  if (!h) return SDPC_ERR_INVALID_ARG;
+  h->truncate = on != 0;
+  return SDPC_OK;
+}
+
 sdpc_status sdpc_set_timing(sdpc_handle h, int32_t on) {
   if (!h) return SDPC_ERR_INVALID_ARG;
   h->timing = on != 0;
@@ -503,6 +509,8 @@ sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t 
     return SDPC_ERR_NOT_PD;
   }
   h->have_y = true;
+  // the truncated sweep needs every vertex as a RHS (single rank) and B = X-hat o Y^{-1} (max-cut)
+  h->trunc_active = h->truncate && h->cons.maxcut && h->nranks == 1 && h->d.nrhs == h->S.n;
   h->launches += launch_inverse_panels(h, st);
   if (h->timing) CK(cudaEventRecord(h->ev[4], st));
   h->launches += launch_scm(h, B, ldb, st);
@@ -520,7 +528,7 @@ sdpc_status sdpc_scm_build(sdpc_handle h, const double* y_E, double* B, int64_t 
 sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t ncols, double* X_out, double* Y_out,
                                      void* stream) {
   if (!h || !cols || ncols < 1 || !X_out || !Y_out) return SDPC_ERR_INVALID_ARG;
-  if (!h->have_y || !h->Xh) return SDPC_ERR_STATE;
+  if (!h->have_y || !h->Xh || h->trunc_active) return SDPC_ERR_STATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<int32_t> cn(ncols);

@@ -107,6 +107,8 @@ struct sdpc_ctx {
   cudaStream_t st2 = nullptr;    // lookahead stream of the SCM Cholesky
   cudaEvent_t evA = nullptr, evB = nullptr;
   bool have_x = false, have_y = false;
+  bool truncate = true;          // allow the truncated backward sweep (max-cut, one rank)
+  bool trunc_active = false;     // the last sdpc_scm_build used it
   int64_t last_info = 0;
   bool timing = true;
   double times[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -28,6 +28,7 @@ __device__ __forceinline__ double pm(const double* __restrict__ M, const int32_t
   return M[((size_t)(s >> 5) * n + row) * kPanelW + (s & 31)];
 }
 
+template <bool TRUNC>
 __global__ void __launch_bounds__(256) scm_maxcut_kernel(int n, int m, const double* __restrict__ Xh,
                                                          const double* __restrict__ Yh,
                                                          const int32_t* __restrict__ rhs,
@@ -35,13 +36,14 @@ __global__ void __launch_bounds__(256) scm_maxcut_kernel(int n, int m, const dou
                                                          const double* __restrict__ aval,
                                                          const int32_t* __restrict__ col_cons, double* B,
                                                          int64_t ldb, Grid g) {
-  __shared__ int32_t lcol[kPanelW];
+  __shared__ int32_t lcol[kPanelW], lvtx[kPanelW];
   __shared__ double lval[kPanelW];
   const int P = blockIdx.y;
   if (threadIdx.x < kPanelW) {
     const int v = rhs[P * kPanelW + threadIdx.x];
     const int l = v >= 0 ? col_cons[v] : -1;
     lcol[threadIdx.x] = l;
+    lvtx[threadIdx.x] = v;
     lval[threadIdx.x] = l >= 0 ? aval[l] : 0.0;
   }
   __syncthreads();
@@ -52,6 +54,25 @@ __global__ void __launch_bounds__(256) scm_maxcut_kernel(int n, int m, const dou
   double* Bk = B + g.lrow(k);
   const double2* xr = reinterpret_cast<const double2*>(Xh + ((size_t)P * n + i) * kPanelW);
   const double2* yr = reinterpret_cast<const double2*>(Yh + ((size_t)P * n + i) * kPanelW);
+  if (TRUNC) {
+    // truncated solves: column v of the panel is valid at rows i >= v only; the pair {k, l} is taken
+    // from the panel of the smaller elimination index and written to the lower triangle of B
+    if (i < lvtx[0] || lvtx[0] < 0) return;
+#pragma unroll 4
+    for (int h = 0; h < kPanelW / 2; ++h) {
+      const double2 x = xr[h], y = yr[h];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 2 * h + e, l = lcol[c];
+        if (l >= 0 && i >= lvtx[c]) {
+          const double v = ak * lval[c] * (e ? x.y : x.x) * (e ? y.y : y.x);
+          if (k >= l) B[k + (size_t)l * ldb] = v;
+          else B[l + (size_t)k * ldb] = v;
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll 4
   for (int h = 0; h < kPanelW / 2; ++h) {
     const double2 x = xr[h], y = yr[h];
@@ -143,7 +164,12 @@ int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st) {
   if (c.maxcut) {
     if (h->d.npanels == 0) return 0;
     dim3 grid((m + 255) / 256, h->d.npanels);
-    scm_maxcut_kernel<<<grid, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B, ldb, g);
+    if (h->trunc_active)
+      scm_maxcut_kernel<true><<<grid, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B, ldb,
+                                                     g);
+    else
+      scm_maxcut_kernel<false><<<grid, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B,
+                                                      ldb, g);
     return 1;
   }
   int nl = 0;

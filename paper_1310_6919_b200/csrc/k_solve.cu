@@ -38,6 +38,7 @@ struct SolveArgs {
   const int32_t* border;   // backward task order: top supernodes (level order), then subtrees (preorder)
   const int32_t* sub_ptr;  // [nsub+1] offsets of the subtrees in border (starting at ntop)
   int32_t ntop, nsub;
+  int32_t trunc;  // max-cut, one rank: the backward sweep stops below the panel's smallest RHS
   const int32_t* sparent;
   const double* Lp[2];
   const double* D[2];
@@ -351,7 +352,7 @@ __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, 
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double smem_solve[];
   double* Vs = smem_solve;                                                          // chunk of S rows
   double* Bs = smem_solve + kChunk * kVs;                                           // 2 staged K-chunks
@@ -364,6 +365,9 @@ __global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveAr
   const double* __restrict__ D = a.D[fac];
   double* X = a.out[fac] + (size_t)P * n * kPanelW;
   const int myrhs = a.rhs[P * kPanelW + lane];  // this lane's RHS: e_{myrhs} (all-zero column if -1)
+  // truncated backward (SURVEY §8(a) note): only rows i >= pmin of this panel are read later, and
+  // row i of x depends only on rows > i, so supernodes entirely below pmin are skipped
+  const int pmin = a.trunc ? a.rhs[P * kPanelW] : -1;
   const int32_t* __restrict__ rowind = a.rowind;
 
   const int nwords = (a.nsuper + 31) / 32;
@@ -431,6 +435,7 @@ __global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveAr
   for (int it = 0; it < a.ntop; ++it) {
     const int r = a.border[it];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
+    if (f + s - 1 < pmin) continue;  // uniform over the CTA
     const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
     const double* Lr = Lp + a.panel_off[r];
     const int32_t* U = rowind + a.colptr[f] + s;
@@ -447,6 +452,7 @@ __global__ void __launch_bounds__(kSolveThreads, 3) inverse_panel_kernel(SolveAr
     for (int it = a.sub_ptr[q]; it < a.sub_ptr[q + 1]; ++it) {
       const int r = a.border[it];
       const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
+      if (f + s - 1 < pmin) continue;
       const bool onpath = (inreach[r >> 5] >> (r & 31)) & 1u;
       const double* Lr = Lp + a.panel_off[r];
       const int32_t* U = rowind + a.colptr[f] + s;
@@ -479,6 +485,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
   a.sub_ptr = h->d.sub_ptr;
   a.ntop = h->S.ntop;
   a.nsub = (int32_t)h->S.sub_ptr.size() - 1;
+  a.trunc = h->trunc_active ? 1 : 0;
   a.sparent = h->d.sparent;
   a.Lp[0] = h->Lx;
   a.Lp[1] = h->Ly;

@@ -35,6 +35,7 @@ _SIGS = [
     ("sdpc_iteration_host", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
     ("sdpc_set_timing", C.c_int, [_P, C.c_int32]),
+    ("sdpc_set_truncation", C.c_int, [_P, C.c_int32]),
     ("sdpc_launch_count", C.c_int64, [_P]),
     ("sdpc_fp64_peak", C.c_int, [C.c_int32, C.c_double, _P, _P]),
     ("sdpc_destroy", C.c_int, [_P]),
@@ -194,6 +195,9 @@ class Handle:
         t = (C.c_double * 8)()
         self._check(lib().sdpc_get_phase_times(self.h, t), "sdpc_get_phase_times")
         return list(t)
+
+    def set_truncation(self, on):
+        self._check(lib().sdpc_set_truncation(self.h, int(bool(on))), "sdpc_set_truncation")
 
     def set_timing(self, on):
         self._check(lib().sdpc_set_timing(self.h, int(bool(on))), "sdpc_set_timing")

@@ -289,3 +289,62 @@ def test_cholesky_random_spd_ragged(m, pad):
     Ro = CH.potrf_lower(Bh)
     assert rel(np.tril(Rg), Ro) < TOL_R
     assert CH.backward_error(Bh, np.tril(Rg)) < 1e-14
+
+
+@pytest.mark.parametrize("kind", ["maxcut_nd", "theta"])
+def test_inverse_columns_free_check(kind):
+    """(a1)+(b) at once: x_p = X-hat e_p restricted to the pattern equals X-bar (max-det completion,
+    SURVEY §8(c) free check), and Y y_q = e_q; full (untruncated) columns via sdpc_get_inverse_columns."""
+    from paper_1310_6919_b200 import Handle
+    inst = small(kind)
+    dev = torch.device("cuda:0")
+    h = Handle.from_instance(inst)
+    h.set_truncation(False)
+    x = torch.from_numpy(inst.xbar).to(dev)
+    y = torch.from_numpy(inst.y).to(dev)
+    h.factor_xinv(x)
+    Bt = torch.zeros((inst.m, inst.m), dtype=torch.float64, device=dev)
+    h.scm_build(y, Bt)
+    n = inst.n
+    cols = np.arange(0, n, max(1, n // 17), dtype=np.int32)
+    Xo = torch.zeros((len(cols), n), dtype=torch.float64, device=dev)   # column c at Xo[c]
+    Yo = torch.zeros_like(Xo)
+    h.get_inverse_columns(cols, Xo, Yo)
+    Xo, Yo = Xo.cpu().numpy(), Yo.cpu().numpy()
+    perm = np.asarray(inst.perm)
+    iperm = np.argsort(perm)
+    Ydense = np.zeros((n, n))
+    for j in range(n):
+        for e in range(inst.colptr[j], inst.colptr[j + 1]):
+            i = inst.rowind[e]
+            a, b = perm[i], perm[j]
+            Ydense[a, b] = Ydense[b, a] = inst.y[e]
+    for ci, p in enumerate(cols):
+        jp = iperm[p]                               # elimination index of column p
+        # pattern entries of column p (both triangles): X-hat_ip = X-bar_ip
+        for j in range(n):
+            for e in range(inst.colptr[j], inst.colptr[j + 1]):
+                i = inst.rowind[e]
+                if j == jp:
+                    assert abs(Xo[ci][perm[i]] - inst.xbar[e]) < 1e-11 * (1 + abs(inst.xbar[e]))
+                elif i == jp:
+                    assert abs(Xo[ci][perm[j]] - inst.xbar[e]) < 1e-11 * (1 + abs(inst.xbar[e]))
+        r = Ydense @ Yo[ci]
+        r[p] -= 1.0
+        assert np.max(np.abs(r)) < 1e-11
+
+
+def test_truncated_and_full_sweeps_agree():
+    """max-cut: the truncated backward sweep (default) and the full one give the same B."""
+    from paper_1310_6919_b200 import Handle
+    inst = small("maxcut_nd")
+    dev = torch.device("cuda:0")
+    out = []
+    for tr in (True, False):
+        h = Handle.from_instance(inst)
+        h.set_truncation(tr)
+        h.factor_xinv(torch.from_numpy(inst.xbar).to(dev))
+        Bt = torch.full((inst.m, inst.m), float("nan"), dtype=torch.float64, device=dev)
+        h.scm_build(torch.from_numpy(inst.y).to(dev), Bt)
+        out.append(np.tril(Bt.T.cpu().numpy()))
+    assert rel(out[0], out[1]) < 1e-14
