@@ -390,6 +390,11 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   if (h->evA) cudaEventDestroy(h->evA);
   if (h->evB) cudaEventDestroy(h->evB);
   if (h->st2) cudaStreamDestroy(h->st2);
+  for (int i = 0; i < 4; ++i) {
+    if (h->side[i]) cudaStreamDestroy(h->side[i]);
+    if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
+  }
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   delete h;
   return SDPC_OK;
 }

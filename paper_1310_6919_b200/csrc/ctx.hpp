@@ -105,6 +105,9 @@ struct sdpc_ctx {
   double* pinned_out = nullptr;  // pinned host staging (m)
   double* potrf_ws = nullptr;    // inverses of the diagonal blocks (2 x nb x nb, double-buffered)
   cudaStream_t st2 = nullptr;    // lookahead stream of the SCM Cholesky
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // concurrent (a1) size classes
+  cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr;
   cudaEvent_t evA = nullptr, evB = nullptr;
   bool have_x = false, have_y = false;
   bool truncate = true;          // allow the truncated backward sweep (max-cut, one rank)

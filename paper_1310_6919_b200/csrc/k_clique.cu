@@ -431,7 +431,26 @@ int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
   a.vals = xbar;
   a.Lp = h->Lx;
   a.D = h->Dx;
-  return launch_classes<true>(a, h->a1cls, st);
+  // the cliques are independent (Algorithm 1 works clique by clique): the size classes run
+  // concurrently on side streams, so the many small cliques fill the SMs the few big ones leave idle
+  if (!h->side[0]) {
+    for (int i = 0; i < 4; ++i) {
+      cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+  }
+  cudaEventRecord(h->fork_ev, st);
+  int n = 0;
+  for (int q = 0; q < (int)h->a1cls.size() && q < 4; ++q) {
+    cudaStreamWaitEvent(h->side[q], h->fork_ev, 0);
+    std::vector<CliqueClass> one(1, h->a1cls[q]);
+    n += launch_classes<true>(a, one, h->side[q]);
+    one[0].d_sn = nullptr;  // not owned here
+    cudaEventRecord(h->side_ev[q], h->side[q]);
+    cudaStreamWaitEvent(st, h->side_ev[q], 0);
+  }
+  return n;
 }
 
 int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st) {

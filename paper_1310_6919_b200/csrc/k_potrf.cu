@@ -50,25 +50,22 @@ __device__ __noinline__ int warp_chol_inv32(double* Ab, double (*Tinv)[33], int 
   for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * kLdD] : 0.0;
   int fail = -1;
   double rinv = 0.0;  // lane j: 1 / L[j][j]
-  // the scaled column is broadcast through shared memory (Tinv's first row is free until the
-  // inverse is written): one STS + (31 - j) broadcast LDS per column instead of 2 (32 - j) SHFL
-  double* colbuf = &Tinv[0][0];
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
-    if (lane == j) colbuf[32] = row[j];
-    __syncwarp();
-    const double d = colbuf[32];
+    const double d = __shfl_sync(0xffffffffu, row[j], j);
     if (fail < 0 && !(d > 0.0)) fail = j;
-    const double rl = rsqrt_nr(d);
-    const double lj = row[j] * rl;  // L[lane][j] (lane >= j)
-    if (lane == j) rinv = rl;
-    if (lane >= j) row[j] = lj;
-    colbuf[lane] = lj;
-    __syncwarp();
+    const double rl = rsqrt_nr(d);  // MUFU seed + Newton: no out-of-line slow path on the chain
+    if (lane == j) {
+      row[j] = d * rl;
+      rinv = rl;
+    } else if (lane > j) {
+      row[j] *= rl;
+    }
 #pragma unroll
-    for (int k = j + 1; k < 32; ++k)
-      if (lane >= k) row[k] -= lj * colbuf[k];
-    __syncwarp();
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, row[j], k);
+      if (lane >= k) row[k] -= row[j] * lkj;
+    }
   }
   if (fail >= 0) return fail;
 #pragma unroll
