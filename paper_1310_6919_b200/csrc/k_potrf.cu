@@ -627,19 +627,32 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
       subpanel(k0 + kNB, w - kNB, s);
     }
   };
-  panel(0, st);
+  // Schedule (depth-2 lookahead).  s2 (high priority) carries the critical path: for every outer
+  // step k, ucol(k) = panel k's update of block column k+1, then panel(k+1).  st carries the bulk:
+  // urest(k) = panel k's update of block column k+2 first (uA, so ucol(k+1) can start as soon as it
+  // is done) and then of everything beyond (uB).  Events: evB = "panel(k+1) done" (st waits before
+  // urest(k+1) reads its L21), evA = "uA(k) done" (s2 waits before ucol(k+1)).
+  cudaEventRecord(h->evA, st);  // input ready
+  cudaStreamWaitEvent(s2, h->evA, 0);
+  panel(0, s2);
+  cudaEventRecord(h->evB, s2);
+  cudaStreamWaitEvent(st, h->evB, 0);
+  bool have_uA = false;
   for (int64_t k0 = 0; k0 < m; k0 += kOuter) {
     const int w = (int)std::min<int64_t>(kOuter, m - k0);
     const int64_t base = k0 + w;
     const int rows = (int)(m - base);
     if (rows <= 0) break;
     const int T = (rows + kTile - 1) / kTile;
-    const int ncol = std::min<int>(T, kOuter / kTile);  // tile columns of the next outer block column
-    upd(kModeUpdCols, k0, w, base, 0, ncol, st);
-    cudaEventRecord(h->evA, st);
-    cudaStreamWaitEvent(s2, h->evA, 0);
+    const int ncol = std::min<int>(T, kOuter / kTile);           // tile columns of block column k+1
+    const int ncol2 = std::min<int>(T - ncol, kOuter / kTile);   // ... of block column k+2
+    // critical path on s2: ucol(k) (needs uA(k-1): block column k+1 complete up to step k-1)
+    if (have_uA) cudaStreamWaitEvent(s2, h->evA, 0);
+    upd(kModeUpdCols, k0, w, base, 0, ncol, s2);
     panel(base, s2);
     cudaEventRecord(h->evB, s2);
+    // bulk on st: urest(k) = uA(k) + uB(k)
+    have_uA = false;
     if (T > ncol) {
       if (tim) {
         if ((int)h->upd_ev.size() < 2 * (nu + 1)) {
@@ -651,7 +664,10 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
         }
         cudaEventRecord(h->upd_ev[2 * nu], st);
       }
-      upd(kModeUpdTri, k0, w, base, ncol, 0, st);
+      upd(kModeUpdCols, k0, w, base, ncol, ncol + ncol2, st);
+      cudaEventRecord(h->evA, st);
+      have_uA = true;
+      if (T > ncol + ncol2) upd(kModeUpdTri, k0, w, base, ncol + ncol2, 0, st);
       if (tim) cudaEventRecord(h->upd_ev[2 * nu + 1], st);
       ++nu;
       // algorithmic flops of this update: the lower triangle of the trailing block past the next
@@ -659,7 +675,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
       const double r2 = (double)(rows - ncol * kTile);
       fl += r2 * (r2 + 1.0) * (double)w;
     }
-    cudaStreamWaitEvent(st, h->evB, 0);
+    cudaStreamWaitEvent(st, h->evB, 0);  // urest(k+1) reads panel k+1
   }
   if (flops_upd) *flops_upd = fl;
   if (n_upd) *n_upd = nu;
