@@ -25,12 +25,15 @@ namespace sdpc {
 
 constexpr int kNB = 128;         // panel width
 constexpr int kTile = 128;        // GEMM tile rows (BM); also the row/column unit of the tile grids
-constexpr int kBN = 64;           // GEMM tile columns
+constexpr int kBN = 128;          // GEMM tile columns (64: 2 CTAs/SM of 8 warps; 128: 1 CTA/SM of 16 warps)
+constexpr int kR = kTile / kBN;   // GEMM column tiles per 128-column unit
 constexpr int kBK = 32;           // k-chunk per pipeline stage (8 DMMA k-steps per barrier)
 constexpr int kStages = 2;
 constexpr int kLdA = kTile + 4;   // smem row strides (doubles): conflict-free fragment loads
 constexpr int kLdB = kBN + 4;
-constexpr int kGemmThreads = 256;  // 8 warps x (32 x 32), 2 CTAs per SM
+constexpr int kGemmThreads = 4 * kBN;  // 4 x (kBN/32) warps of 32 x 32
+constexpr int kGemmCtasPerSm = kBN == 64 ? 2 : 1;
+constexpr int kTrsmThreads = 256;  // in-place panel solve: 8 warps x (64 x 32)
 
 __device__ __forceinline__ double neg(double x) {  // sign flip on the integer pipe
   return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
@@ -258,7 +261,7 @@ enum { kModeTrsm = 0, kModeUpdCols = 1, kModeUpdTri = 2, kModeRect = 3, kModeDis
 
 
 template <int MODE, bool AL16>
-__global__ void __launch_bounds__(kGemmThreads, 2) gemm_nt_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(GemmArgs g) {
   if (*g.err != kNoError) return;
   extern __shared__ double sm[];
   double* As = sm;                          // [kStages][kBK][kLdA]
@@ -296,18 +299,19 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_nt_kernel(GemmArgs g) {
     int t = blockIdx.x, bi, bj;  // bj in 64-column units
     if (MODE == kModeUpdCols) {  // column-major over the 128-columns [c0, c1), two halves each
       int c = g.c0;
-      while (t >= 2 * (T - c)) {
-        t -= 2 * (T - c);
+      while (t >= kR * (T - c)) {
+        t -= kR * (T - c);
         ++c;
       }
-      bi = c + (t >> 1);
-      bj = 2 * c + (t & 1);
-    } else {  // row-major over the lower triangle of 128-columns [c0, T): row r has 2r + 2 halves
-      int r = (int)((sqrt(4.0 * t + 1.0) - 1.0) * 0.5);
-      while (r * (r + 1) > t) --r;
-      while ((r + 1) * (r + 2) <= t) ++r;
+      bi = c + t / kR;
+      bj = kR * c + t % kR;
+    } else {  // row-major over the lower triangle of 128-columns [c0, T): row r has kR (r + 1) tiles
+      const int tt = t / kR;
+      int r = (int)((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
+      while (r * (r + 1) / 2 > tt) --r;
+      while ((r + 1) * (r + 2) / 2 <= tt) ++r;
       bi = g.c0 + r;
-      bj = 2 * g.c0 + (t - r * (r + 1));
+      bj = kR * g.c0 + (t - kR * (r * (r + 1) / 2));
     }
     Ab = g.A + (size_t)bi * kTile;
     Bb = g.Bm + (size_t)bj * kBN;
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_nt_kernel(GemmArgs g) {
 // before writing any of them, and owns all <= 128 output columns of those rows).  128 x 128 tile,
 // 8 warps x (64 x 32), same pipeline as the update kernel.
 template <bool AL16>
-__global__ void __launch_bounds__(kGemmThreads, 1) trsm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kTrsmThreads, 1) trsm_kernel(GemmArgs g) {
   if (*g.err != kNoError) return;
   extern __shared__ double sm[];
   double* As = sm;                          // [kStages][kBK][kLdA]
@@ -438,8 +442,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) trsm_kernel(GemmArgs g) {
     double* as = As + stage * kBK * kLdA;
     double* bs = Bs + stage * kBK * kLdA;
 #pragma unroll
-    for (int q = 0; q < (kBK * kTile) / kGemmThreads; ++q) {
-      const int cid = tid + q * kGemmThreads;
+    for (int q = 0; q < (kBK * kTile) / kTrsmThreads; ++q) {
+      const int cid = tid + q * kTrsmThreads;
       const int kk = cid / kTile, rp = cid % kTile;
       const bool kv = (k0 + kk) < g.K;
       if (AL16) {
@@ -514,8 +518,8 @@ template <int MODE>
 static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g, cudaStream_t st) {
   if (grid.x == 0 || grid.y == 0) return;
   if (MODE == kModeTrsm) {  // in place: one CTA owns all (<= 128) columns of its rows
-    if (al16) trsm_kernel<true><<<dim3(grid.x), kGemmThreads, trsm_smem(), st>>>(g);
-    else trsm_kernel<false><<<dim3(grid.x), kGemmThreads, trsm_smem(), st>>>(g);
+    if (al16) trsm_kernel<true><<<dim3(grid.x), kTrsmThreads, trsm_smem(), st>>>(g);
+    else trsm_kernel<false><<<dim3(grid.x), kTrsmThreads, trsm_smem(), st>>>(g);
     return;
   }
   if (al16) gemm_nt_kernel<MODE, true><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
@@ -588,11 +592,11 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     u.err = d_err;
     int grid = 0;
     if (mode == kModeUpdCols) {
-      for (int c = c0; c < std::min(c1, T); ++c) grid += 2 * (T - c);
+      for (int c = c0; c < std::min(c1, T); ++c) grid += kR * (T - c);
       launch_gemm<kModeUpdCols>(al16, dim3(grid), u, s);
     } else {
       const int S = T - c0;
-      grid = S > 0 ? S * (S + 1) : 0;
+      grid = S > 0 ? kR * S * (S + 1) / 2 : 0;
       launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s);
     }
     if (grid > 0) ++launches;
