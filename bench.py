@@ -424,10 +424,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (not used by the driver): run the N-rank schedule on fewer GPUs with gloo, e.g.
+    # SDPC_BENCH_BACKEND=gloo SDPC_BENCH_DEVICE=0 torchrun --nproc-per-node 2 bench.py --gpus 2
+    backend = os.environ.get("SDPC_BENCH_BACKEND", "nccl")
+    if "SDPC_BENCH_DEVICE" in os.environ:
+        local_rank = int(os.environ["SDPC_BENCH_DEVICE"])
     if world > 1 and args.impl == "ours":
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.distributed.init_process_group(backend)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:

@@ -426,6 +426,15 @@ static int launch_classes(const CliqueArgs& a, const std::vector<CliqueClass>& c
   return n;
 }
 
+static void ensure_side_streams(sdpc_ctx* h) {
+  if (h->side[0]) return;
+  for (int i = 0; i < 4; ++i) {
+    cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+}
+
 int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
   CliqueArgs a = base_args(h);
   a.vals = xbar;
@@ -433,13 +442,7 @@ int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
   a.D = h->Dx;
   // the cliques are independent (Algorithm 1 works clique by clique): the size classes run
   // concurrently on side streams, so the many small cliques fill the SMs the few big ones leave idle
-  if (!h->side[0]) {
-    for (int i = 0; i < 4; ++i) {
-      cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
-    }
-    cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
-  }
+  ensure_side_streams(h);
   cudaEventRecord(h->fork_ev, st);
   int n = 0;
   for (int q = 0; q < (int)h->a1cls.size() && q < 4; ++q) {
@@ -458,8 +461,28 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st) {
   a.vals = y;
   a.Lp = h->Ly;
   a.D = h->Dy;
+  // levels are sequential (a front needs its children's update matrices); the size classes of one
+  // level are independent fronts and run concurrently on the side streams
+  ensure_side_streams(h);
   int n = 0;
-  for (const auto& lev : h->a2lev) n += launch_classes<false>(a, lev, st);
+  for (const auto& lev : h->a2lev) {
+    int used = 0;
+    for (const auto& k : lev) used += k.sn.empty() ? 0 : 1;
+    if (used <= 1) {
+      n += launch_classes<false>(a, lev, st);
+      continue;
+    }
+    cudaEventRecord(h->fork_ev, st);
+    for (int q = 0; q < (int)lev.size() && q < 4; ++q) {
+      if (lev[q].sn.empty()) continue;
+      cudaStreamWaitEvent(h->side[q], h->fork_ev, 0);
+      std::vector<CliqueClass> one(1, lev[q]);
+      n += launch_classes<false>(a, one, h->side[q]);
+      one[0].d_sn = nullptr;
+      cudaEventRecord(h->side_ev[q], h->side[q]);
+      cudaStreamWaitEvent(st, h->side_ev[q], 0);
+    }
+  }
   return n;
 }
 

@@ -25,7 +25,7 @@ namespace sdpc {
 
 constexpr int kNB = 128;         // panel width
 constexpr int kTile = 128;        // GEMM tile rows (BM); also the row/column unit of the tile grids
-constexpr int kBN = 128;          // GEMM tile columns (64: 2 CTAs/SM of 8 warps; 128: 1 CTA/SM of 16 warps)
+constexpr int kBN = 64;           // GEMM tile columns (64: 2 CTAs/SM of 8 warps; 128: 1 CTA/SM of 16 warps)
 constexpr int kR = kTile / kBN;   // GEMM column tiles per 128-column unit
 constexpr int kBK = 32;           // k-chunk per pipeline stage (8 DMMA k-steps per barrier)
 constexpr int kStages = 2;
