@@ -285,6 +285,45 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     reach_ptr[P + 1] = (int32_t)reach_sn.size();
   }
 
+  // ---- staged-rows accumulation (one rank, every vertex a RHS slot in order): per small constraint
+  // the distinct vertices V_l of its entries and, per entry, the positions of p and q in V_l;
+  // large constraints whose entries are all diagonal ("diag-large", e.g. A_1 = I) as dense weights
+  std::vector<int32_t> vptr(m + 1, 0), vlist, eloc(ci.size() * 2, 0);
+  std::vector<uint8_t> diag_large(m, 0);
+  std::vector<double> wdiag;
+  std::vector<int32_t> dlist;
+  int nvmax = 0;
+  for (int32_t l = 0; l < m; ++l) {
+    if (is_large[l]) {
+      bool diag = true;
+      for (int64_t e2 = cptr[l]; e2 < cptr[l + 1]; ++e2) diag = diag && ci[e2] == cj[e2];
+      if (diag) {
+        diag_large[l] = 1;
+        dlist.push_back(l);
+        const size_t o = wdiag.size();
+        wdiag.resize(o + n, 0.0);
+        for (int64_t e2 = cptr[l]; e2 < cptr[l + 1]; ++e2) wdiag[o + ci[e2]] += cv[e2];
+      }
+      vptr[l + 1] = (int32_t)vlist.size();
+      continue;
+    }
+    std::vector<int32_t> vs;
+    for (int64_t e2 = cptr[l]; e2 < cptr[l + 1]; ++e2) vs.push_back(ci[e2]);
+    std::sort(vs.begin(), vs.end());
+    vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+    for (int64_t e2 = cptr[l]; e2 < cptr[l + 1]; ++e2) {
+      eloc[2 * e2] = (int32_t)(std::lower_bound(vs.begin(), vs.end(), cj[e2]) - vs.begin());      // p = ej
+      eloc[2 * e2 + 1] = (int32_t)(std::lower_bound(vs.begin(), vs.end(), ci[e2]) - vs.begin());  // q = ei
+    }
+    nvmax = std::max<int>(nvmax, (int)vs.size());
+    vlist.insert(vlist.end(), vs.begin(), vs.end());
+    vptr[l + 1] = (int32_t)vlist.size();
+  }
+  const size_t rows_smem = (size_t)2 * nvmax * n * sizeof(double);
+  h->cons.rows_mode = !maxcut && nranks == 1 && nrhs == n && nvmax > 0 && rows_smem <= kRowsSmemCap;
+  h->cons.nvmax = nvmax;
+  h->cons.ndiag = (int32_t)dlist.size();
+
   // ---- upload
   DevSym& d = h->d;
   d.n = n;
@@ -341,6 +380,12 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(cs.vrow, vrow);
   UP(cs.aval, aval);
   UP(cs.col_cons, col_cons);
+  UP(cs.vptr, vptr);
+  UP(cs.vlist, vlist);
+  UP(cs.eloc, eloc);
+  UP(cs.diag_large, diag_large);
+  UP(cs.wdiag, wdiag);
+  UP(cs.dlist, dlist);
 #undef UP
 #define AL(dst, cnt)                                    \
   if ((e = dalloc(&(dst), (cnt))) != cudaSuccess) { \
@@ -376,7 +421,8 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
                   d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, h->d_ws_off,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
-                  h->cons.vrow, h->cons.aval, h->cons.col_cons, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
+                  h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
+                  h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
                   h->d_err, h->d_ok, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
   for (void* p : ptrs)
     if (p) cudaFree(p);

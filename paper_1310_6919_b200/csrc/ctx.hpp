@@ -72,7 +72,17 @@ struct DevCons {
   int32_t* vrow = nullptr;      // [m] elimination row of constraint k's vertex
   double* aval = nullptr;       // [m] value a_k
   int32_t* col_cons = nullptr;  // [n] constraint index whose vertex is elimination column j, or -1
+  // staged-rows accumulation (one rank, identity slots): see k_scm.cu
+  bool rows_mode = false;
+  int32_t nvmax = 0, ndiag = 0;
+  int32_t* vptr = nullptr;      // [m+1] distinct vertices V_l of small constraint l
+  int32_t* vlist = nullptr;
+  int32_t* eloc = nullptr;      // [2 * entries] positions of p (= ej) and q (= ei) in V_l
+  uint8_t* diag_large = nullptr;  // [m] large constraint with diagonal entries only
+  double* wdiag = nullptr;      // [ndiag][n] their weights
+  int32_t* dlist = nullptr;     // [ndiag] their constraint ids
 };
+constexpr size_t kRowsSmemCap = 200 * 1024;
 
 }  // namespace sdpc
 

@@ -119,6 +119,86 @@ __global__ void __launch_bounds__(256) scm_general_kernel(int n, int m, const do
   }
 }
 
+// Staged-rows accumulation (one rank, RHS slot = vertex): by symmetry X-hat_{jp} = row p of X-hat at
+// column j, and row p of the panel-major array is npanels contiguous 256-byte pieces.  The CTA of
+// column l stages the rows of X-hat and Y^{-1} of the distinct vertices V_l of A_l in shared memory
+// (coalesced), then every B_kl, k >= l, is sum_e v_e sum_f w_f Xr[p_f][j_e] Yr[q_f][i_e] with
+// shared-memory reads only; the entries (K, l) with K a diagonal-only large constraint (A_1 = I of
+// the theta SDP) are the block reductions sum_f w_f sum_t wK[t] Xr[p_f][t] Yr[q_f][t].
+__global__ void __launch_bounds__(256) scm_rows_kernel(int n, int m, const double* __restrict__ Xh,
+                                                       const double* __restrict__ Yh,
+                                                       const int64_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ ei,
+                                                       const int32_t* __restrict__ ej,
+                                                       const double* __restrict__ ev,
+                                                       const uint8_t* __restrict__ is_large,
+                                                       const int32_t* __restrict__ vptr,
+                                                       const int32_t* __restrict__ vlist,
+                                                       const int32_t* __restrict__ eloc,
+                                                       const double* __restrict__ wdiag,
+                                                       const int32_t* __restrict__ dlist, int ndiag, double* B,
+                                                       int64_t ldb) {
+  extern __shared__ double rows_sm[];
+  __shared__ int32_t sp[kMaxSmall], sq[kMaxSmall];
+  __shared__ double sw[kMaxSmall];
+  __shared__ double red[8];
+  const int l = blockIdx.x;
+  if (is_large[l]) return;
+  const int nv = vptr[l + 1] - vptr[l];
+  double* Xr = rows_sm;             // [nv][n]
+  double* Yr = rows_sm + (size_t)nv * n;
+  const int tid = threadIdx.x;
+  for (int a = 0; a < nv; ++a) {
+    const int v = vlist[vptr[l] + a];
+    for (int t = tid; t < n; t += blockDim.x) {
+      const size_t o = ((size_t)(t >> 5) * n + v) * kPanelW + (t & 31);
+      Xr[(size_t)a * n + t] = Xh[o];
+      Yr[(size_t)a * n + t] = Yh[o];
+    }
+  }
+  const int64_t lb = ptr[l];
+  const int nl = (int)(ptr[l + 1] - lb);
+  for (int t = tid; t < nl; t += blockDim.x) {
+    sp[t] = eloc[2 * (lb + t)];
+    sq[t] = eloc[2 * (lb + t) + 1];
+    sw[t] = ev[lb + t];
+  }
+  __syncthreads();
+  for (int k = l + tid; k < m; k += blockDim.x) {
+    if (is_large[k]) continue;
+    double sum = 0.0;
+    for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e) {
+      const int i = ei[e], j = ej[e];
+      const double v = ev[e];
+      double inner = 0.0;
+      for (int t = 0; t < nl; ++t) inner += sw[t] * Xr[(size_t)sp[t] * n + j] * Yr[(size_t)sq[t] * n + i];
+      sum += v * inner;
+    }
+    B[k + (size_t)l * ldb] = sum;
+  }
+  // pairs with the diagonal-only large constraints
+  for (int dq = 0; dq < ndiag; ++dq) {
+    const int K = dlist[dq];
+    const double* wk = wdiag + (size_t)dq * n;
+    double acc = 0.0;
+    for (int t = tid; t < n; t += blockDim.x) {
+      double inner = 0.0;
+      for (int f = 0; f < nl; ++f) inner += sw[f] * Xr[(size_t)sp[f] * n + t] * Yr[(size_t)sq[f] * n + t];
+      acc += wk[t] * inner;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double sacc = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) sacc += red[w];
+      const int hi = K > l ? K : l, lo = K > l ? l : K;
+      B[hi + (size_t)lo * ldb] = sacc;
+    }
+    __syncthreads();
+  }
+}
+
 // Pairs (K large, l any): the entry lands in column c = min(K, l), row r = max(K, l); the sum runs
 // over A_r's entries (k role) and A_c's entries (l role), reading only the RHS of column c.
 __global__ void __launch_bounds__(512) scm_large_kernel(int n, int m, const double* __restrict__ Xh,
@@ -129,12 +209,14 @@ __global__ void __launch_bounds__(512) scm_large_kernel(int n, int m, const doub
                                                         const int32_t* __restrict__ ej,
                                                         const double* __restrict__ ev,
                                                         const int32_t* __restrict__ large,
-                                                        const uint8_t* __restrict__ is_large, double* B,
-                                                        int64_t ldb, Grid g) {
+                                                        const uint8_t* __restrict__ is_large,
+                                                        const uint8_t* __restrict__ diag_large, bool rows_mode,
+                                                        double* B, int64_t ldb, Grid g) {
   __shared__ double red[32];
   const int l = blockIdx.x;
   const int K = large[blockIdx.y];
   if (is_large[l] && l > K) return;  // large x large pairs computed once (l <= K)
+  if (rows_mode && !is_large[l] && diag_large[K]) return;  // done by scm_rows_kernel
   const int r = K > l ? K : l, c = K > l ? l : K;
   if (!g.own_row(r) || !g.own_col(c)) return;
   const int64_t rb = ptr[r], nr = ptr[r + 1] - rb;
@@ -173,13 +255,24 @@ int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st) {
     return 1;
   }
   int nl = 0;
-  scm_general_kernel<<<m, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.slot_of, c.ptr, c.ei, c.ej, c.ev, c.is_large, B,
-                                        ldb, g);
+  if (c.rows_mode) {
+    const size_t smem = (size_t)2 * c.nvmax * n * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(scm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowsSmemCap);
+      attr = true;
+    }
+    scm_rows_kernel<<<m, 256, smem, st>>>(n, m, h->Xh, h->Yh, c.ptr, c.ei, c.ej, c.ev, c.is_large, c.vptr, c.vlist,
+                                          c.eloc, c.wdiag, c.dlist, c.ndiag, B, ldb);
+  } else {
+    scm_general_kernel<<<m, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.slot_of, c.ptr, c.ei, c.ej, c.ev, c.is_large, B,
+                                          ldb, g);
+  }
   ++nl;
   if (c.nlarge > 0) {
     dim3 grid(m, c.nlarge);
     scm_large_kernel<<<grid, 512, 0, st>>>(n, m, h->Xh, h->Yh, h->d.slot_of, c.ptr, c.ei, c.ej, c.ev, c.large,
-                                           c.is_large, B, ldb, g);
+                                           c.is_large, c.diag_large, c.rows_mode, B, ldb, g);
     ++nl;
   }
   return nl;
