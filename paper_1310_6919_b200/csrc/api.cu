@@ -386,6 +386,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(cs.diag_large, diag_large);
   UP(cs.wdiag, wdiag);
   UP(cs.dlist, dlist);
+  h->diag_ids = dlist;
 #undef UP
 #define AL(dst, cnt)                                    \
   if ((e = dalloc(&(dst), (cnt))) != cudaSuccess) { \
@@ -400,6 +401,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   AL(h->upd, (size_t)S.upd_total);
   AL(h->d_err, 1);
   AL(h->d_ok, 1);
+  AL(h->pair_ws, (size_t)std::max(1, npanels) * ((n + 1023) / 1024));
   AL(h->potrf_ws, 2 * 128 * 128);
 #undef AL
   for (auto& ev : h->ev) cudaEventCreate(&ev);
@@ -423,7 +425,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
                   h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
-                  h->d_err, h->d_ok, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
+                  h->d_err, h->d_ok, h->pair_ws, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->pinned_in) cudaFreeHost(h->pinned_in);

@@ -91,6 +91,8 @@ struct sdpc_ctx {
   int nranks = 1, rank = 0;
   sdpc::Grid grid;                 // 2D block-cyclic process grid of B
   std::vector<int32_t> slot_of_host;  // host copy of DevSym::slot_of
+  std::vector<int32_t> diag_ids;      // host copy of DevCons::dlist
+  double* pair_ws = nullptr;          // partial sums of the diagonal-large pair reductions
   int64_t mloc = 0, nloc = 0;      // local rows / columns of B on this rank
   sdpc::Symbolic S;
   sdpc::DevSym d;

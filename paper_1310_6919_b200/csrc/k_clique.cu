@@ -159,25 +159,42 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
       // one 8 x 8 lower tile per warp task (m8n8k4 DMMA, K = jw), C read-modify-written in place
       const int lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
       const int nb8 = (nr + 7) >> 3, ntile = nb8 * (nb8 + 1) / 2;
-      for (int t = wid; t < ntile; t += NT / 32) {
-        int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-        while (ti * (ti + 1) / 2 > t) --ti;
-        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-        const int tj = t - ti * (ti + 1) / 2;
-        const int i = r0 + ti * 8 + g8, j = r0 + tj * 8 + 2 * t4;
-        const bool iv = i < c;
-        double c0 = (iv && j < c && j <= i) ? A[i + (size_t)j * ld] : 0.0;
-        double c1 = (iv && j + 1 < c && j + 1 <= i) ? A[i + (size_t)(j + 1) * ld] : 0.0;
-        const int ia = r0 + ti * 8 + g8, ja = r0 + tj * 8 + g8;
-#pragma unroll 4
-        for (int k0 = 0; k0 < jw; k0 += 4) {
-          const int k = k0 + t4;
-          const double av = (ia < c && k < jw) ? P[ia + (size_t)k * ld] : 0.0;
-          const double bv = (ja < c && k < jw) ? P[ja + (size_t)k * ld] : 0.0;
-          dmma_8x8x4(c0, c1, -av, bv);
+      constexpr int kB = 4;  // tiles per warp batch: their C loads are in flight together
+      for (int t0 = wid * kB; t0 < ntile; t0 += (NT / 32) * kB) {
+        double c0[kB], c1[kB];
+        int ii[kB], jj[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int t = t0 + b;
+          int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+          while (ti * (ti + 1) / 2 > t) --ti;
+          while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+          const int tj = t - ti * (ti + 1) / 2;
+          ii[b] = t < ntile ? r0 + ti * 8 : c;  // c: empty tile
+          jj[b] = r0 + tj * 8;
+          const int i = ii[b] + g8, j = jj[b] + 2 * t4;
+          const bool iv = i < c;
+          c0[b] = (iv && j < c && j <= i) ? A[i + (size_t)j * ld] : 0.0;
+          c1[b] = (iv && j + 1 < c && j + 1 <= i) ? A[i + (size_t)(j + 1) * ld] : 0.0;
         }
-        if (iv && j < c && j <= i) A[i + (size_t)j * ld] = c0;
-        if (iv && j + 1 < c && j + 1 <= i) A[i + (size_t)(j + 1) * ld] = c1;
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int ia = ii[b] + g8, ja = jj[b] + g8;
+#pragma unroll 4
+          for (int k0 = 0; k0 < jw; k0 += 4) {
+            const int k = k0 + t4;
+            const double av = (ia < c && k < jw) ? P[ia + (size_t)k * ld] : 0.0;
+            const double bv = (ja < c && k < jw) ? P[ja + (size_t)k * ld] : 0.0;
+            dmma_8x8x4(c0[b], c1[b], -av, bv);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int i = ii[b] + g8, j = jj[b] + 2 * t4;
+          const bool iv = i < c;
+          if (iv && j < c && j <= i) A[i + (size_t)j * ld] = c0[b];
+          if (iv && j + 1 < c && j + 1 <= i) A[i + (size_t)(j + 1) * ld] = c1[b];
+        }
       }
     }
     __syncthreads();

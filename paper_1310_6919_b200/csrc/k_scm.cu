@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(512) scm_large_kernel(int n, int m, const doub
   const int l = blockIdx.x;
   const int K = large[blockIdx.y];
   if (is_large[l] && l > K) return;  // large x large pairs computed once (l <= K)
-  if (rows_mode && !is_large[l] && diag_large[K]) return;  // done by scm_rows_kernel
+  if (rows_mode && diag_large[K] && (!is_large[l] || diag_large[l])) return;  // rows / pair kernels
   const int r = K > l ? K : l, c = K > l ? l : K;
   if (!g.own_row(r) || !g.own_col(c)) return;
   const int64_t rb = ptr[r], nr = ptr[r + 1] - rb;
@@ -236,6 +236,50 @@ __global__ void __launch_bounds__(512) scm_large_kernel(int n, int m, const doub
     sum = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (lane == 0) B[g.lrow(r) + g.lcol(c) * ldb] = sum;
+  }
+}
+
+// Pairs of diagonal-only large constraints (K, K'): B = sum_{t,s} wK[t] wK'[s] X-hat_ts Y^{-1}_ts, a
+// reduction over all n^2 entries of X-hat o Y^{-1} (e.g. B_11 = trace(X-hat Y^{-1}) for A_1 = I).
+// Grid (panels, row chunks), one partial sum per block, summed in a fixed order by the second kernel.
+constexpr int kPairRows = 1024;
+__global__ void __launch_bounds__(256) scm_diag_pair_partial(int n, const double* __restrict__ Xh,
+                                                             const double* __restrict__ Yh,
+                                                             const int32_t* __restrict__ rhs,
+                                                             const double* __restrict__ wa,
+                                                             const double* __restrict__ wb, double* partial) {
+  __shared__ double red[8];
+  const int P = blockIdx.x, r0 = blockIdx.y * kPairRows;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int v = rhs[P * kPanelW + lane];
+  const double wv = v >= 0 ? wb[v] : 0.0;
+  double acc = 0.0;
+  for (int i = r0 + wid; i < min(n, r0 + kPairRows); i += 8) {
+    const size_t o = ((size_t)P * n + i) * kPanelW + lane;
+    acc += wa[i] * Xh[o] * Yh[o];
+  }
+  acc *= wv;
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+__global__ void scm_diag_pair_finish(const double* __restrict__ partial, int np, double* dst) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += partial[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    *dst = s;
   }
 }
 
@@ -274,6 +318,18 @@ int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st) {
     scm_large_kernel<<<grid, 512, 0, st>>>(n, m, h->Xh, h->Yh, h->d.slot_of, c.ptr, c.ei, c.ej, c.ev, c.large,
                                            c.is_large, c.diag_large, c.rows_mode, B, ldb, g);
     ++nl;
+  }
+  if (c.rows_mode && c.ndiag > 0) {
+    const int np = h->d.npanels, nchunk = (n + kPairRows - 1) / kPairRows;
+    for (int a = 0; a < c.ndiag; ++a)
+      for (int b = a; b < c.ndiag; ++b) {
+        const int K = h->diag_ids[a], K2 = h->diag_ids[b];
+        const int hi = K > K2 ? K : K2, lo = K > K2 ? K2 : K;
+        scm_diag_pair_partial<<<dim3(np, nchunk), 256, 0, st>>>(n, h->Xh, h->Yh, h->d.rhs, c.wdiag + (size_t)a * n,
+                                                                 c.wdiag + (size_t)b * n, h->pair_ws);
+        scm_diag_pair_finish<<<1, 256, 0, st>>>(h->pair_ws, np * nchunk, B + hi + (size_t)lo * ldb);
+        nl += 2;
+      }
   }
   return nl;
 }
