@@ -107,7 +107,7 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
 // every warp task is one 8 x 8 output tile (8 rows of the supernode x 8 RHS) with K running over
 // the panel rows / columns.  The triangular L_SS parts run on 128-row chunks staged in shared
 // memory (16-row diagonal blocks in registers of one warp, the rest of the chunk by all warps).
-constexpr int kBigS = 16;     // supernodes with at least this many columns take this path
+constexpr int kBigS = kTopMinS;  // supernodes with at least this many columns take this path
 constexpr int kChunk = 128;   // rows of S per shared-memory chunk
 constexpr int kVs = 36;       // chunk row stride (doubles): conflict-free 8-RHS fragment reads
 
@@ -183,7 +183,9 @@ __device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, cons
       __syncthreads();
       for (int t = b0 + bw + wid; t < w; t += nw) {
         double v = Vs[t * kVs + lane];
-        for (int j = 0; j < bw; ++j) v -= Lr[(t0 + t) + (size_t)(t0 + b0 + j) * c] * Vs[(b0 + j) * kVs + lane];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < bw) v -= Lr[(t0 + t) + (size_t)(t0 + b0 + j) * c] * Vs[(b0 + j) * kVs + lane];
         Vs[t * kVs + lane] = v;
       }
       __syncthreads();
@@ -310,7 +312,9 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
       __syncthreads();
       for (int t = wid; t < b0; t += nw) {
         double v = Vs[t * kVs + lane];
-        for (int j = 0; j < bw; ++j) v -= Lr[(t0 + b0 + j) + (size_t)(t0 + t) * c] * Vs[(b0 + j) * kVs + lane];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < bw) v -= Lr[(t0 + b0 + j) + (size_t)(t0 + t) * c] * Vs[(b0 + j) * kVs + lane];
         Vs[t * kVs + lane] = v;
       }
       __syncthreads();

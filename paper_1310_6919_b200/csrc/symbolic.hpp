@@ -14,6 +14,10 @@
 
 namespace sdpc {
 
+// Supernodes with at least this many columns go to the CTA-wide (tensor-core) part of the backward
+// solve (k_solve.cu kBigS); they and their ancestors form the "top" of the task order.
+constexpr int kTopMinS = 16;
+
 struct Symbolic {
   int32_t n = 0, m = 0;
   std::vector<int32_t> perm, iperm, parent;
