@@ -284,18 +284,15 @@ std::string analyse(Symbolic& S, int32_t n, int32_t m, const int64_t* a_ptr, con
     for (int32_t r = 0; r < ns; ++r)
       if (S.sparent[r] < 0) total += w[r];
     const int64_t wmax = std::max<int64_t>(1, total / 96);
-    // top = heavy subtrees, plus every supernode wide enough for the CTA-wide tensor-core path
-    // (|S| >= kTopMinS) and all of their ancestors (the top is processed before the subtrees)
+    // top = heavy subtrees (CTA-wide tensor-core path, level order); the rest are subtrees, one warp
+    // each (a wide supernode alone in a light subtree, e.g. a block-arrow leaf, stays on a warp: many
+    // such leaves run in parallel that way)
     std::vector<char> is_top(ns, 0);
-    for (int32_t r = ns - 1; r >= 0; --r)  // parents have larger ids: mark, then pull up below
-      if (w[r] > wmax || S.sns[r] >= kTopMinS) is_top[r] = 1;
-    for (int32_t r = 0; r < ns; ++r)
-      if (is_top[r])
-        for (int32_t a = S.sparent[r]; a >= 0 && !is_top[a]; a = S.sparent[a]) is_top[a] = 1;
     std::vector<int32_t> roots;
     for (int32_t r = 0; r < ns; ++r) {
       const int32_t p = S.sparent[r];
-      if (!is_top[r] && (p < 0 || is_top[p])) roots.push_back(r);
+      if (w[r] > wmax) is_top[r] = 1;
+      else if (p < 0 || w[p] > wmax) roots.push_back(r);
     }
     S.border.clear();
     for (size_t lv = 0; lv + 1 < S.dlev_ptr.size(); ++lv) {

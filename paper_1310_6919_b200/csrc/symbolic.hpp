@@ -14,8 +14,8 @@
 
 namespace sdpc {
 
-// Supernodes with at least this many columns go to the CTA-wide (tensor-core) part of the backward
-// solve (k_solve.cu kBigS); they and their ancestors form the "top" of the task order.
+// Supernodes with at least this many columns take the CTA-wide (tensor-core) code of the forward
+// solve and of the top of the backward solve (k_solve.cu kBigS).
 constexpr int kTopMinS = 16;
 
 struct Symbolic {

@@ -2,6 +2,7 @@
 set -x
 ./tools/mb_warpchol > gpurun_out/mb.log 2>&1; echo mb $?
 timeout 120 python tools/time_tiles.py > gpurun_out/tiles.log 2>&1; echo tiles $?
+timeout 120 python tools/yardstick_potrf.py 10000 > gpurun_out/yardstick.log 2>&1; echo yard $?
 timeout 900 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build $?
 timeout 240 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1 || { echo smoke failed; exit 3; }
 timeout 1500 python -m pytest tests -m gpu -q -x --durations=10 > gpurun_out/pytest_gpu.log 2>&1; echo pytest $?
