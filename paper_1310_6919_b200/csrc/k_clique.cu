@@ -353,20 +353,41 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
     F[idx] = (j < s && i >= j) ? a.vals[colptr[f + j] + (i - j)] : 0.0;
   }
   __syncthreads();
-  // extend-add of the children's update matrices (sequential over children: deterministic)
-  for (int q = a.child_ptr[r]; q < a.child_ptr[r + 1]; ++q) {
-    const int ch = a.child_list[q];
-    const int uc = a.snc[ch] - a.sns[ch];
-    const int32_t* rel = a.relind + a.relind_off[ch];
-    const double* Uc = a.upd + a.upd_off[ch];
-    // lower triangle only, one warp per column ib (coalesced U_c column, relative indices)
+  // extend-add of the children's update matrices.  Two children or fewer: one child at a time (warp
+  // per column, deterministic order).  More (e.g. the block-arrow border front with 200 children):
+  // all (child, column) pairs at once with FP64 atomic adds (summation order then varies, reading #13)
+  {
+    const int c0 = a.child_ptr[r], c1 = a.child_ptr[r + 1];
     const int lane = tid & 31, wid = tid >> 5;
-    for (int ib = wid; ib < uc; ib += NT / 32) {
-      double* Fc = F + (size_t)rel[ib] * c;
-      const double* Ucol = Uc + (size_t)ib * uc;
-      for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
+    if (c1 - c0 <= 2) {
+      for (int q = c0; q < c1; ++q) {
+        const int ch = a.child_list[q];
+        const int uc = a.snc[ch] - a.sns[ch];
+        const int32_t* rel = a.relind + a.relind_off[ch];
+        const double* Uc = a.upd + a.upd_off[ch];
+        for (int ib = wid; ib < uc; ib += NT / 32) {
+          double* Fc = F + (size_t)rel[ib] * c;
+          const double* Ucol = Uc + (size_t)ib * uc;
+          for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
+        }
+        __syncthreads();
+      }
+    } else {
+      int base = 0;
+      for (int q = c0; q < c1; ++q) {  // flat (child, column) work list, one warp per item
+        const int ch = a.child_list[q];
+        const int uc = a.snc[ch] - a.sns[ch];
+        const int32_t* rel = a.relind + a.relind_off[ch];
+        const double* Uc = a.upd + a.upd_off[ch];
+        for (int ib = (wid - base % (NT / 32) + NT / 32) % (NT / 32); ib < uc; ib += NT / 32) {
+          double* Fc = F + (size_t)rel[ib] * c;
+          const double* Ucol = Uc + (size_t)ib * uc;
+          for (int ia = ib + lane; ia < uc; ia += 32) atomicAdd(Fc + rel[ia], Ucol[ia]);
+        }
+        base += uc;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   // Cholesky of the |S_r| pivot columns (L~ = L D^{1/2}) with the Schur complement in F_UU
   double* panel = ((size_t)c * 32 * sizeof(double) <= (size_t)pbytes) ? smem : F + (size_t)c * c + (size_t)c * s;

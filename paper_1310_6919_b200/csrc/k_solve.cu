@@ -53,7 +53,6 @@ __device__ __forceinline__ double& xrow(double* X, int row, int lane) { return X
 template <int kCh>
 __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int c, int s, int f,
                                               const int32_t* __restrict__ U, double* X, int lane, bool onpath) {
-  const int u = c - s;
   for (int t1 = s; t1 > 0; t1 -= kCh) {
     const int t0 = t1 > kCh ? t1 - kCh : 0;
     const int w = t1 - t0;
@@ -61,14 +60,14 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
 #pragma unroll
     for (int j = 0; j < kCh; ++j) acc[j] = (j < w && onpath) ? xrow(X, f + t0 + j, lane) : 0.0;
     const double* Lc = Lr + (size_t)t0 * c;  // Lc[i + j*c] = L[i, t0+j]
-    // U rows in blocks of 32: indices and L values loaded coalesced by the warp, broadcast by
-    // shuffles; 8 independent row loads in flight
-    for (int q0 = 0; q0 < u; q0 += 32) {
-      const int nq = min(32, u - q0);
-      const int myrow = lane < nq ? U[q0 + lane] : 0;
+    // gathered rows t1..c-1 (the rows of S after the chunk, final by now, then U) in blocks of 32:
+    // indices and L values loaded coalesced by the warp, broadcast by shuffles; 8 row loads in flight
+    for (int q0 = t1; q0 < c; q0 += 32) {
+      const int nq = min(32, c - q0);
+      const int myrow = lane < nq ? (q0 + lane < s ? f + q0 + lane : U[q0 + lane - s]) : 0;
       double lv[kCh];
 #pragma unroll
-      for (int j = 0; j < kCh; ++j) lv[j] = (j < w && lane < nq) ? Lc[s + q0 + lane + (size_t)j * c] : 0.0;
+      for (int j = 0; j < kCh; ++j) lv[j] = (j < w && lane < nq) ? Lc[q0 + lane + (size_t)j * c] : 0.0;
       for (int k0 = 0; k0 < nq; k0 += 8) {
         double xq[8];
 #pragma unroll
@@ -82,12 +81,6 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
           for (int j = 0; j < kCh; ++j) acc[j] -= __shfl_sync(0xffffffffu, lv[j], k0 + k) * xq[k];
         }
       }
-    }
-    for (int tp = t1; tp < s; ++tp) {
-      const double xq = xrow(X, f + tp, lane);
-#pragma unroll
-      for (int j = 0; j < kCh; ++j)
-        if (j < w) acc[j] -= Lc[tp + (size_t)j * c] * xq;
     }
 #pragma unroll
     for (int j = kCh - 1; j >= 0; --j) {
