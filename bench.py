@@ -39,6 +39,11 @@ CONFIG_TEXT = {
 FP64_OVER_BF16 = 45.0 / 2250.0
 FALLBACK_BF16 = dict(burst=1590.0, sustained=1400.0)   # B200_PROFILING.md fallback
 FALLBACK_HBM = 6650.0
+# ncu --set full of one gemm_nt_kernel<UpdTri> launch on configs[1] (4290 tiles of 128 x 64, K = 256,
+# 1.80e10 flops): dram__bytes_read.sum + dram__bytes_write.sum = 292.2 MB + 220.2 MB.
+UPD_BYTES_PER_FLOP = (292.243456e6 + 220.247040e6) / (4290 * 128 * 64 * 2 * 256)
+UPD_TRAFFIC_SOURCE = ("profiles/r01/ncu/update_UpdTri_128x64_full.txt: 512.5 MB DRAM read+write for one launch "
+                      "of 1.80e10 flops, scaled by the step's update flops")
 
 
 def peaks():
@@ -223,7 +228,11 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches_per_step": launches / args.steps,
         "roofline": {"kernel": "gemm_nt_kernel<kModeUpdTri> (SCM Cholesky trailing update, K = 256, DMMA)",
                      "bound": "tensor", "achieved": achieved, "peak": fp64_peak_tf, "unit": "TFLOP/s",
-                     "frac": (achieved / fp64_peak_tf) if achieved else None, "traffic": None,
+                     "frac": (achieved / fp64_peak_tf) if achieved else None,
+                     # DRAM bytes of the step's update launches, from the measured bytes/flop of one
+                     # profiled launch (ncu --set full; C read once + written once per tile, panel in L2)
+                     "traffic": UPD_BYTES_PER_FLOP * upd_flops,
+                     "traffic_source": UPD_TRAFFIC_SOURCE,
                      "peak_source": peak_src,
                      "launches_per_step": n_upd, "flops_per_step": upd_flops,
                      "fp64_microbench_tflops": {"dmma": dmma, "dfma": dfma}},

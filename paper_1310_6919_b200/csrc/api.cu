@@ -194,6 +194,28 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   if (build_classes(h->a1cls, all, b1, ws_off, pb) != cudaSuccess) return fail(SDPC_ERR_OOM);
   const int nh = (int)S.hlev_ptr.size() - 1;
   h->a2lev.resize(nh);
+  // (a2) fronts in the global workspace with many children: their extend-add runs beforehand as a
+  // grid-wide kernel (one CTA per child, FP64 atomics) instead of inside the front's own CTA
+  std::vector<uint8_t> pre(ns, 0);
+  std::vector<int32_t> pre_ptr(nh + 1, 0), pre_child, pre_parent, zero_ptr(nh + 1, 0), zero_list;
+  for (int lv = 0; lv < nh; ++lv) {
+    for (int32_t q = S.hlev_ptr[lv]; q < S.hlev_ptr[lv + 1]; ++q) {
+      const int32_t r = S.hlev_sn[q];
+      const int32_t nch = S.child_ptr[r + 1] - S.child_ptr[r];
+      if (ws_off[r] >= 0 && nch > 2) {
+        pre[r] = 1;
+        zero_list.push_back(r);
+        for (int32_t cq = S.child_ptr[r]; cq < S.child_ptr[r + 1]; ++cq) {
+          pre_child.push_back(S.child_list[cq]);
+          pre_parent.push_back(r);
+        }
+      }
+    }
+    pre_ptr[lv + 1] = (int32_t)pre_child.size();
+    zero_ptr[lv + 1] = (int32_t)zero_list.size();
+  }
+  h->pre_ptr = pre_ptr;
+  h->zero_ptr = zero_ptr;
   for (int lv = 0; lv < nh; ++lv) {
     std::vector<int32_t> mem(S.hlev_sn.begin() + S.hlev_ptr[lv], S.hlev_sn.begin() + S.hlev_ptr[lv + 1]);
     std::stable_sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
@@ -367,6 +389,10 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(d.slot_of, slot_of);
   h->slot_of_host = slot_of;
   UP(h->d_ws_off, ws_off);
+  UP(h->d_pre, pre);
+  UP(h->d_pre_child, pre_child);
+  UP(h->d_pre_parent, pre_parent);
+  UP(h->d_zero_list, zero_list);
   DevCons& cs = h->cons;
   cs.maxcut = maxcut;
   cs.m = m;
@@ -421,7 +447,8 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   DevSym& d = h->d;
   void* ptrs[] = {d.colptr, d.rowind, d.super_ptr, d.snc, d.sns, d.sparent, d.panel_off, d.e2p, d.umap_off,
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
-                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, h->d_ws_off,
+                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, h->d_ws_off, h->d_pre, h->d_pre_child,
+                  h->d_pre_parent, h->d_zero_list,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
                   h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,

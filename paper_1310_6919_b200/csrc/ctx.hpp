@@ -101,6 +101,12 @@ struct sdpc_ctx {
   std::vector<std::vector<sdpc::CliqueClass>> a2lev;
   double* ws = nullptr;          // global workspace for large cliques ((a1) and (a2))
   int64_t* d_ws_off = nullptr;   // per supernode offset into ws (doubles), -1 if smem class
+  // (a2) pre-pass extend-add for global fronts with many children (per height level)
+  uint8_t* d_pre = nullptr;
+  int32_t* d_pre_child = nullptr;
+  int32_t* d_pre_parent = nullptr;
+  int32_t* d_zero_list = nullptr;
+  std::vector<int32_t> pre_ptr, zero_ptr;
   double* Lx = nullptr;          // X factor panels
   double* Dx = nullptr;
   double* Ly = nullptr;          // Y factor panels

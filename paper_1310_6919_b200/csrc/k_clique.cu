@@ -41,6 +41,7 @@ struct CliqueArgs {
   const int32_t* relind;
   const int64_t* upd_off;
   double* upd;
+  const uint8_t* pre;  // front already holds its children's extend-add (pre-pass)
 };
 
 constexpr unsigned kFullMask = 0xffffffffu;
@@ -347,17 +348,21 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
   const int tid = threadIdx.x;
   const int64_t* __restrict__ colptr = a.colptr;
 
-  // frontal matrix: pivot columns from Y on E, the U x U block starts at zero
+  // frontal matrix: pivot columns from Y on E, the U x U block starts at zero (pre-pass fronts
+  // already hold the extend-add of their children: add instead of overwrite)
+  const bool pre = a.pre[r] != 0;
   for (int idx = tid; idx < c * c; idx += NT) {
     const int i = idx % c, j = idx / c;
-    F[idx] = (j < s && i >= j) ? a.vals[colptr[f + j] + (i - j)] : 0.0;
+    const double yv = (j < s && i >= j) ? a.vals[colptr[f + j] + (i - j)] : 0.0;
+    if (pre) F[idx] += yv;
+    else F[idx] = yv;
   }
   __syncthreads();
   // extend-add of the children's update matrices.  Two children or fewer: one child at a time (warp
   // per column, deterministic order).  More (e.g. the block-arrow border front with 200 children):
   // all (child, column) pairs at once with FP64 atomic adds (summation order then varies, reading #13)
   {
-    const int c0 = a.child_ptr[r], c1 = a.child_ptr[r + 1];
+    const int c0 = pre ? 0 : a.child_ptr[r], c1 = pre ? 0 : a.child_ptr[r + 1];
     const int lane = tid & 31, wid = tid >> 5;
     if (c1 - c0 <= 2) {
       for (int q = c0; q < c1; ++q) {
@@ -416,6 +421,32 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
   }
 }
 
+// (a2) pre-pass for global fronts with many children: zero the front, then one CTA per child adds
+// its update matrix (lower triangle, warp per column) with FP64 atomics
+__global__ void zero_fronts_kernel(const int32_t* __restrict__ list, const int64_t* __restrict__ ws_off,
+                                   const int32_t* __restrict__ snc, double* ws) {
+  const int r = list[blockIdx.x];
+  const int64_t c = snc[r];
+  double* F = ws + ws_off[r];
+  for (int64_t i = threadIdx.x; i < c * c; i += blockDim.x) F[i] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) extend_add_kernel(CliqueArgs a, const int32_t* __restrict__ child,
+                                                         const int32_t* __restrict__ parent) {
+  const int ch = child[blockIdx.x], r = parent[blockIdx.x];
+  const int c = a.snc[r];
+  double* F = a.ws + a.ws_off[r];
+  const int uc = a.snc[ch] - a.sns[ch];
+  const int32_t* rel = a.relind + a.relind_off[ch];
+  const double* Uc = a.upd + a.upd_off[ch];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int ib = wid; ib < uc; ib += blockDim.x / 32) {
+    double* Fc = F + (size_t)rel[ib] * c;
+    const double* Ucol = Uc + (size_t)ib * uc;
+    for (int ia = ib + lane; ia < uc; ia += 32) atomicAdd(Fc + rel[ia], Ucol[ia]);
+  }
+}
+
 static CliqueArgs base_args(sdpc_ctx* h) {
   CliqueArgs a{};
   a.super_ptr = h->d.super_ptr;
@@ -434,6 +465,7 @@ static CliqueArgs base_args(sdpc_ctx* h) {
   a.relind = h->d.relind;
   a.upd_off = h->d.upd_off;
   a.upd = h->upd;
+  a.pre = h->d_pre;
   return a;
 }
 
@@ -503,7 +535,15 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st) {
   // level are independent fronts and run concurrently on the side streams
   ensure_side_streams(h);
   int n = 0;
-  for (const auto& lev : h->a2lev) {
+  for (int lvi = 0; lvi < (int)h->a2lev.size(); ++lvi) {
+    const auto& lev = h->a2lev[lvi];
+    const int z0 = h->zero_ptr[lvi], z1 = h->zero_ptr[lvi + 1];
+    if (z1 > z0) {
+      zero_fronts_kernel<<<z1 - z0, 256, 0, st>>>(h->d_zero_list + z0, h->d_ws_off, h->d.snc, h->ws);
+      const int p0 = h->pre_ptr[lvi], p1 = h->pre_ptr[lvi + 1];
+      extend_add_kernel<<<p1 - p0, 256, 0, st>>>(a, h->d_pre_child + p0, h->d_pre_parent + p0);
+      n += 2;
+    }
     int used = 0;
     for (const auto& k : lev) used += k.sn.empty() ? 0 : 1;
     if (used <= 1) {
