@@ -191,9 +191,20 @@ sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const doubl
                               int64_t k1, int32_t K, void* stream);
 
 /*
+ * sdpc_iteration - the whole hot path on DEVICE buffers in one call (what bench.py times):
+ * (a1) sdpc_factor_xinv and (a2) the factorisation of Y run concurrently on two streams (they are
+ * independent), then (b), (c) and (d) as in sdpc_scm_build + sdpc_scm_cholesky, with a single
+ * synchronisation at the end.  Arguments as for those calls (B: m x m column-major, ldb >= m).
+ * Errors: NOT_PD with sdpc_last_info() = the index of the first failing phase in the order (a1)
+ * clique r, (a2) column j, (d) leading minor k; *info = k only for (d) (else 0).  nranks == 1 only.
+ */
+sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_E, double* B,
+                           int64_t ldb, int32_t* info, void* stream);
+
+/*
  * sdpc_iteration_host - the whole hot path from HOST buffers (what a host-side PDIPM driver
  * calls once per iteration): copies xbar_E and y_E (HOST [nnzE]) to the device, runs
- * factor_xinv -> scm_build -> scm_cholesky into a handle-owned B, and copies back
+ * sdpc_iteration into a handle-owned B, and copies back
  * rdiag (HOST [m], the diagonal of R; NULL allowed) and info (HOST).
  */
 sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const double* y_E,

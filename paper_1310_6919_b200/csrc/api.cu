@@ -420,12 +420,13 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     return fail(SDPC_ERR_OOM);                        \
   }
   AL(h->ws, (size_t)ws_total);
+  AL(h->ws2, (size_t)ws_total);
   AL(h->Lx, (size_t)S.panel_total);
   AL(h->Ly, (size_t)S.panel_total);
   AL(h->Dx, (size_t)n);
   AL(h->Dy, (size_t)n);
   AL(h->upd, (size_t)S.upd_total);
-  AL(h->d_err, 1);
+  AL(h->d_err, 4);  // [0] default / (a1), [1] (a2), [2] (d) in sdpc_iteration
   AL(h->d_ok, 1);
   AL(h->pair_ws, (size_t)std::max(1, npanels) * ((n + 1023) / 1024));
   AL(h->potrf_ws, 2 * 128 * 128);
@@ -451,7 +452,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   h->d_pre_parent, h->d_zero_list,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
-                  h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
+                  h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->ws2, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
                   h->d_err, h->d_ok, h->pair_ws, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -465,11 +466,16 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   if (h->evA) cudaEventDestroy(h->evA);
   if (h->evB) cudaEventDestroy(h->evB);
   if (h->st2) cudaStreamDestroy(h->st2);
-  for (int i = 0; i < 4; ++i) {
-    if (h->side[i]) cudaStreamDestroy(h->side[i]);
-    if (h->side_ev[i]) cudaEventDestroy(h->side_ev[i]);
-  }
+  for (int q = 0; q < 2; ++q)
+    for (int i = 0; i < 4; ++i) {
+      if (h->sides[q][i]) cudaStreamDestroy(h->sides[q][i]);
+      if (h->sides_ev[q][i]) cudaEventDestroy(h->sides_ev[q][i]);
+    }
   if (h->fork_ev) cudaEventDestroy(h->fork_ev);
+  if (h->fork_ev2) cudaEventDestroy(h->fork_ev2);
+  if (h->st3) cudaStreamDestroy(h->st3);
+  if (h->it_fork) cudaEventDestroy(h->it_fork);
+  if (h->it_join) cudaEventDestroy(h->it_join);
   delete h;
   return SDPC_OK;
 }
@@ -658,6 +664,77 @@ sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* in
   return SDPC_OK;
 }
 
+sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_E, double* B, int64_t ldb,
+                           int32_t* info, void* stream) {
+  if (!h || !xbar_E || !y_E || !B || !info || ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
+  if (h->nranks != 1) return SDPC_ERR_STATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t dense = std::max<size_t>(1, (size_t)h->d.npanels * h->S.n * kPanelW);
+  if (!h->Xh) {
+    CK(dalloc(&h->Xh, dense));
+    CK(dalloc(&h->Yh, dense));
+  }
+  if (!h->st3) {
+    CK(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->it_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->it_join, cudaEventDisableTiming));
+  }
+  h->have_x = h->have_y = false;
+  CK(cudaMemsetAsync(h->d_err, 0x7f, 3 * sizeof(int32_t), st));
+  if (h->timing) CK(cudaEventRecord(h->ev[0], st));
+  // (a1) on st and (a2) on st3 concurrently: both are latency-bound walks over the cliques / the
+  // elimination tree with few CTAs in flight, and they do not depend on each other
+  CK(cudaEventRecord(h->it_fork, st));
+  CK(cudaStreamWaitEvent(h->st3, h->it_fork, 0));
+  h->launches += launch_alg1(h, xbar_E, st);
+  h->launches += launch_ldl_y(h, y_E, h->st3, h->d_err + 1, 1);
+  CK(cudaEventRecord(h->it_join, h->st3));
+  CK(cudaStreamWaitEvent(st, h->it_join, 0));
+  if (h->timing) CK(cudaEventRecord(h->ev[1], st));
+  h->trunc_active = h->truncate && h->cons.maxcut && h->nranks == 1 && h->d.nrhs == h->S.n;
+  h->launches += launch_inverse_panels(h, st);
+  if (h->timing) CK(cudaEventRecord(h->ev[4], st));
+  h->launches += launch_scm(h, B, ldb, st);
+  if (h->timing) CK(cudaEventRecord(h->ev[5], st));
+  double fl = 0;
+  int nu = 0;
+  h->launches += potrf_lower(h, B, h->S.m, ldb, h->d_err + 2, st, &fl, &nu, h->potrf_ws);
+  if (h->timing) CK(cudaEventRecord(h->ev[7], st));
+  int32_t fl3[3];
+  CK(cudaMemcpyAsync(fl3, h->d_err, sizeof(fl3), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (h->timing) {
+    h->times[0] = elapsed(h->ev[0], h->ev[1]);  // (a1) || (a2)
+    h->times[1] = 0.0;
+    h->times[2] = elapsed(h->ev[1], h->ev[4]);
+    h->times[3] = elapsed(h->ev[4], h->ev[5]);
+    h->times[4] = elapsed(h->ev[5], h->ev[7]);
+    double tu = 0;
+    for (int i = 0; i < nu; ++i) tu += elapsed(h->upd_ev[2 * i], h->upd_ev[2 * i + 1]);
+    h->times[5] = tu;
+    h->times[6] = nu;
+    h->times[7] = fl;
+  }
+  *info = 0;
+  if (fl3[0] != kNoError) {
+    h->last_info = fl3[0];
+    return SDPC_ERR_NOT_PD;
+  }
+  if (fl3[1] != kNoError) {
+    h->last_info = fl3[1];
+    return SDPC_ERR_NOT_PD;
+  }
+  h->have_x = h->have_y = true;
+  if (fl3[2] != kNoError) {
+    *info = fl3[2];
+    h->last_info = fl3[2];
+    return SDPC_ERR_NOT_PD;
+  }
+  return SDPC_OK;
+}
+
 sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const double* y_E, double* rdiag,
                                 int32_t* info, void* stream) {
   if (!h || !xbar_E || !y_E || !info) return SDPC_ERR_INVALID_ARG;
@@ -677,12 +754,8 @@ sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const doubl
   std::memcpy(h->pinned_in + nnz, y_E, sizeof(double) * nnz);
   CK(cudaMemcpyAsync(h->xin, h->pinned_in, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(h->yin, h->pinned_in + nnz, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
-  sdpc_status s = sdpc_factor_xinv(h, h->xin, stream);
-  if (s != SDPC_OK) return s;
-  s = sdpc_scm_build(h, h->yin, h->Bown, ldb, stream);
-  if (s != SDPC_OK) return s;
-  s = sdpc_scm_cholesky(h, h->Bown, ldb, info, stream);
-  if (s != SDPC_OK && s != SDPC_ERR_NOT_PD) return s;
+  sdpc_status s = sdpc_iteration(h, h->xin, h->yin, h->Bown, ldb, info, stream);
+  if (s != SDPC_OK && !(s == SDPC_ERR_NOT_PD && *info > 0)) return s;
   if (rdiag) {
     h->launches += launch_diag_copy(h->Bown, m, ldb, h->xin, st);
     CK(cudaMemcpyAsync(h->pinned_out, h->xin, sizeof(double) * m, cudaMemcpyDeviceToHost, st));

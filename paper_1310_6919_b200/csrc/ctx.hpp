@@ -99,7 +99,8 @@ struct sdpc_ctx {
   sdpc::DevCons cons;
   std::vector<sdpc::CliqueClass> a1cls, a2cls;  // per-level classes for (a2) are rebuilt per level
   std::vector<std::vector<sdpc::CliqueClass>> a2lev;
-  double* ws = nullptr;          // global workspace for large cliques ((a1) and (a2))
+  double* ws = nullptr;          // global workspace for large cliques of (a1)
+  double* ws2 = nullptr;         // ... and of (a2) (separate: the two may run concurrently)
   int64_t* d_ws_off = nullptr;   // per supernode offset into ws (doubles), -1 if smem class
   // (a2) pre-pass extend-add for global fronts with many children (per height level)
   uint8_t* d_pre = nullptr;
@@ -123,9 +124,13 @@ struct sdpc_ctx {
   double* pinned_out = nullptr;  // pinned host staging (m)
   double* potrf_ws = nullptr;    // inverses of the diagonal blocks (2 x nb x nb, double-buffered)
   cudaStream_t st2 = nullptr;    // lookahead stream of the SCM Cholesky
-  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // concurrent (a1) size classes
+  cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // = sides[0]: (a1) size classes
   cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t fork_ev = nullptr;
+  cudaStream_t sides[2][4] = {};   // [0]: (a1) / (a2) size classes, [1]: (a2) inside sdpc_iteration
+  cudaEvent_t sides_ev[2][4] = {};
+  cudaEvent_t fork_ev = nullptr, fork_ev2 = nullptr;
+  cudaStream_t st3 = nullptr;      // (a2) stream of sdpc_iteration (concurrent with (a1))
+  cudaEvent_t it_fork = nullptr, it_join = nullptr;
   cudaEvent_t evA = nullptr, evB = nullptr;
   bool have_x = false, have_y = false;
   bool truncate = true;          // allow the truncated backward sweep (max-cut, one rank)
@@ -142,7 +147,7 @@ struct sdpc_ctx {
 namespace sdpc {
 // Launchers (each returns number of kernels launched; errors via cudaGetLastError).
 int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st);
-int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st);
+int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err = nullptr, int set = 0);
 int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st);
 int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st);
 int launch_panels_to_E(sdpc_ctx* h, const double* panels, double* E, cudaStream_t st);

@@ -498,11 +498,17 @@ static int launch_classes(const CliqueArgs& a, const std::vector<CliqueClass>& c
 
 static void ensure_side_streams(sdpc_ctx* h) {
   if (h->side[0]) return;
+  for (int q = 0; q < 2; ++q)
+    for (int i = 0; i < 4; ++i) {
+      cudaStreamCreateWithFlags(&h->sides[q][i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&h->sides_ev[q][i], cudaEventDisableTiming);
+    }
   for (int i = 0; i < 4; ++i) {
-    cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&h->side_ev[i], cudaEventDisableTiming);
+    h->side[i] = h->sides[0][i];
+    h->side_ev[i] = h->sides_ev[0][i];
   }
   cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->fork_ev2, cudaEventDisableTiming);
 }
 
 int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
@@ -526,8 +532,10 @@ int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
   return n;
 }
 
-int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st) {
+int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err, int set) {
   CliqueArgs a = base_args(h);
+  a.ws = h->ws2;  // own workspace: (a2) may run concurrently with (a1)
+  if (err) a.err = err;
   a.vals = y;
   a.Lp = h->Ly;
   a.D = h->Dy;
@@ -539,7 +547,7 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st) {
     const auto& lev = h->a2lev[lvi];
     const int z0 = h->zero_ptr[lvi], z1 = h->zero_ptr[lvi + 1];
     if (z1 > z0) {
-      zero_fronts_kernel<<<z1 - z0, 256, 0, st>>>(h->d_zero_list + z0, h->d_ws_off, h->d.snc, h->ws);
+      zero_fronts_kernel<<<z1 - z0, 256, 0, st>>>(h->d_zero_list + z0, h->d_ws_off, h->d.snc, a.ws);
       const int p0 = h->pre_ptr[lvi], p1 = h->pre_ptr[lvi + 1];
       extend_add_kernel<<<p1 - p0, 256, 0, st>>>(a, h->d_pre_child + p0, h->d_pre_parent + p0);
       n += 2;
@@ -550,15 +558,16 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st) {
       n += launch_classes<false>(a, lev, st);
       continue;
     }
-    cudaEventRecord(h->fork_ev, st);
+    cudaEvent_t fk = set ? h->fork_ev2 : h->fork_ev;
+    cudaEventRecord(fk, st);
     for (int q = 0; q < (int)lev.size() && q < 4; ++q) {
       if (lev[q].sn.empty()) continue;
-      cudaStreamWaitEvent(h->side[q], h->fork_ev, 0);
+      cudaStreamWaitEvent(h->sides[set][q], fk, 0);
       std::vector<CliqueClass> one(1, lev[q]);
-      n += launch_classes<false>(a, one, h->side[q]);
+      n += launch_classes<false>(a, one, h->sides[set][q]);
       one[0].d_sn = nullptr;
-      cudaEventRecord(h->side_ev[q], h->side[q]);
-      cudaStreamWaitEvent(st, h->side_ev[q], 0);
+      cudaEventRecord(h->sides_ev[set][q], h->sides[set][q]);
+      cudaStreamWaitEvent(st, h->sides_ev[set][q], 0);
     }
   }
   return n;

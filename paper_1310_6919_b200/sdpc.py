@@ -32,6 +32,7 @@ _SIGS = [
     ("sdpc_potrf_tile", C.c_int, [_P, _P, C.c_int32, C.c_int64, _P, _P, _P]),
     ("sdpc_trsm_panel", C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_int32, _P]),
     ("sdpc_update_tiles", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int32, _P]),
+    ("sdpc_iteration", C.c_int, [_P, _P, _P, _P, C.c_int64, _P, _P]),
     ("sdpc_iteration_host", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
     ("sdpc_set_timing", C.c_int, [_P, C.c_int32]),
@@ -180,6 +181,16 @@ class Handle:
     def update_tiles(self, C_loc, ldc, P, ldp, k1, K, stream=None):
         self._check(lib().sdpc_update_tiles(self.h, _ptr(C_loc), int(ldc), _ptr(P), int(ldp), int(k1), int(K),
                                             _stream(stream)), "sdpc_update_tiles")
+
+    def iteration(self, xbar_E, y_E, B, ldb=None, stream=None, raise_not_pd=True):
+        """(a1) || (a2) -> (b) -> (c) -> (d) on device buffers; returns the Cholesky info."""
+        ldb = self.m if ldb is None else ldb
+        info = C.c_int32(0)
+        st = lib().sdpc_iteration(self.h, _ptr(xbar_E), _ptr(y_E), _ptr(B), int(ldb), C.byref(info), _stream(stream))
+        if st == SDPC_ERR_NOT_PD and not raise_not_pd and info.value > 0:
+            return int(info.value)
+        self._check(st, "sdpc_iteration")
+        return int(info.value)
 
     def iteration_host(self, xbar_E, y_E, rdiag=None, stream=None):
         x = np.ascontiguousarray(xbar_E, dtype=np.float64)

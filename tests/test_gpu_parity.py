@@ -348,3 +348,38 @@ def test_truncated_and_full_sweeps_agree():
         h.scm_build(torch.from_numpy(inst.y).to(dev), Bt)
         out.append(np.tril(Bt.T.cpu().numpy()))
     assert rel(out[0], out[1]) < 1e-14
+
+
+@pytest.mark.parametrize("kind", ["maxcut_nd", "theta", "blockarrow"])
+def test_fused_iteration_matches_separate_calls(kind):
+    """sdpc_iteration ((a1) || (a2), then (b), (c), (d), one sync) = the three separate calls."""
+    from paper_1310_6919_b200 import Handle
+    inst = small(kind)
+    g = run_gpu(inst)
+    dev = torch.device("cuda:0")
+    h = Handle.from_instance(inst)
+    Bt = torch.full((inst.m, inst.m), float("nan"), dtype=torch.float64, device=dev)
+    info = h.iteration(torch.from_numpy(inst.xbar).to(dev), torch.from_numpy(inst.y).to(dev), Bt)
+    assert info == 0
+    R = np.tril(Bt.T.cpu().numpy())
+    assert rel(R, g["R"]) < 1e-13
+    assert np.all(np.isnan(Bt.T.cpu().numpy()[np.triu_indices(inst.m, 1)]))
+
+
+def test_fused_iteration_not_pd_phases():
+    from paper_1310_6919_b200 import Handle, SdpcError
+    inst, _ = three_by_three()
+    dev = torch.device("cuda:0")
+    x = torch.from_numpy(inst.xbar).to(dev)
+    y = torch.from_numpy(inst.y).to(dev)
+    B = torch.zeros((3, 3), dtype=torch.float64, device=dev)
+    xb = x.clone()
+    xb[4] = 0.1                      # clique 1 indefinite -> (a1) fails first
+    with pytest.raises(SdpcError) as e:
+        Handle.from_instance(inst).iteration(xb, y, B)
+    assert e.value.info == 1
+    yb = y.clone()
+    yb[2] = -1.0                     # Y not PD at column 1 -> (a2)
+    with pytest.raises(SdpcError) as e:
+        Handle.from_instance(inst).iteration(x, yb, B)
+    assert e.value.info == 1
