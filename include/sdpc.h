@@ -212,7 +212,9 @@ sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const doubl
 
 /* Per-phase device times (ms) of the last calls, from CUDA events on the call's stream:
  * t[0]=(a1) t[1]=(a2) t[2]=(b) t[3]=(c) t[4]=(d) t[5]=(d) trailing-update kernels only,
- * t[6]=number of (d) trailing-update launches, t[7]=their total algorithmic flops. */
+ * t[6]=number of (d) trailing-update launches, t[7]=their total algorithmic flops.
+ * After sdpc_iteration, where (a1), (a2) and (b) overlap, t[0], t[1], t[2] are the times from the
+ * start of the iteration to the end of (a1), (a2) and (b) respectively. */
 sdpc_status sdpc_get_phase_times(sdpc_handle h, double* t /* [8] */);
 
 /* Enable (1) / disable (0) per-phase event timing (default on; costs a few events per call). */

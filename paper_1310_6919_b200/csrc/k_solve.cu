@@ -39,6 +39,7 @@ struct SolveArgs {
   const int32_t* sub_ptr;  // [nsub+1] offsets of the subtrees in border (starting at ntop)
   int32_t ntop, nsub;
   int32_t trunc;  // max-cut, one rank: the backward sweep stops below the panel's smallest RHS
+  int32_t fac0;   // first factor of this launch (0: X-hat from L, D; 1: Y^{-1} from L_Y, D_Y)
   const int32_t* sparent;
   const double* Lp[2];
   const double* D[2];
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   double* Vs = smem_solve;                                                          // chunk of S rows
   double* Bs = smem_solve + kChunk * kVs;                                           // 2 staged K-chunks
   uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + (kChunk + 2 * kKc) * kVs);  // bitmap
-  const int P = blockIdx.x, fac = blockIdx.y;
+  const int P = blockIdx.x, fac = blockIdx.y + a.fac0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSolveThreads / 32;
   const int n = a.n;
@@ -462,7 +463,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   }
 }
 
-int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
+int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac) {
   SolveArgs a{};
   a.n = h->S.n;
   a.nsuper = h->S.nsuper;
@@ -497,7 +498,8 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st) {
     attr = true;
   }
   if (h->d.npanels == 0) return 0;
-  dim3 grid(h->d.npanels, 2);
+  a.fac0 = fac0;
+  dim3 grid(h->d.npanels, nfac);
   inverse_panel_kernel<<<grid, kSolveThreads, smem, st>>>(a);
   return 1;
 }
