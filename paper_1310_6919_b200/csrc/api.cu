@@ -676,7 +676,11 @@ sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_
     CK(dalloc(&h->Yh, dense));
   }
   if (!h->st3) {
-    CK(cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking));
+    // (a2) is the critical path of the first half (a level-by-level tree walk): highest priority,
+    // so its few CTAs are scheduled ahead of the X-hat solve CTAs that fill the rest of the GPU
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&h->st3, cudaStreamNonBlocking, hi));
     CK(cudaEventCreateWithFlags(&h->it_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->it_join, cudaEventDisableTiming));
   }

@@ -498,9 +498,12 @@ static int launch_classes(const CliqueArgs& a, const std::vector<CliqueClass>& c
 
 static void ensure_side_streams(sdpc_ctx* h) {
   if (h->side[0]) return;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
   for (int q = 0; q < 2; ++q)
     for (int i = 0; i < 4; ++i) {
-      cudaStreamCreateWithFlags(&h->sides[q][i], cudaStreamNonBlocking);
+      // set 1 carries (a2) inside sdpc_iteration: high priority like its parent stream
+      cudaStreamCreateWithPriority(&h->sides[q][i], cudaStreamNonBlocking, q == 1 ? hi : lo);
       cudaEventCreateWithFlags(&h->sides_ev[q][i], cudaEventDisableTiming);
     }
   for (int i = 0; i < 4; ++i) {
