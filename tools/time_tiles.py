@@ -39,3 +39,15 @@ for nb in (128, 256):
     t = timeit(run)
     tc = timeit(lambda: Bt.copy_(B0))
     print(f"potrf_tile nb={nb}: {t - tc:.1f} us per call (copy {tc:.1f} us excluded)")
+
+# standalone trailing-update GEMM (the dominant kernel) through sdpc_update_tiles on a 1 x 1 grid:
+# C[k1:, k1:] (lower) -= P P^T with K = 256
+for m in (4096, 10000):
+    h = scm_handle(m)
+    C = torch.zeros((m, m), dtype=torch.float64, device=dev)      # column-major view: C[j, i]
+    P = torch.randn((256, m), dtype=torch.float64, device=dev)      # panel: row r = global row 256 + r
+    k1 = 256
+    t = timeit(lambda: h.update_tiles(C, m, P, m, k1, 256), reps=10)
+    r = m - k1
+    fl = r * (r + 1) * 256.0
+    print(f"update_tiles m={m} K=256: {t:.1f} us, {fl / (t * 1e-6) / 1e12:.2f} TF/s")
