@@ -236,9 +236,10 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
 
 // ------------------------------------------------------------------ tensor-core GEMM
 // C op= A B^T on 128 x 128 tiles.  TRSM: C = A B^T (acc from zero; B = explicit L11^{-1}).
-// Updates (UPD*, RECT, DIST): the accumulators start as C (loaded straight into registers, so the HBM
-// read of C overlaps the operand pipeline instead of serialising behind the main loop) and the A
-// fragments are negated, so acc = C - A B^T; the epilogue only stores.
+// Updates (UPD*, RECT, DIST): the accumulators start as -C (loaded straight into registers, so the
+// HBM read of C overlaps the operand pipeline instead of serialising behind the main loop), the
+// fragments go from shared memory straight into DMMA (acc = -C + A B^T), and the epilogue stores
+// -acc = C - A B^T.
 struct GemmArgs {
   const double* A;  // element (i, kk) at A[i + kk*lda], i relative to the tile-row base
   int64_t lda;
@@ -378,7 +379,9 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = wn * 32 + b * 8 + 2 * t4 + e;
-        acc[a][b][e] = (UPD && i < na && j < nbv && (!mask || j + doff <= i)) ? Cb[i + (size_t)j * g.ldc] : 0.0;
+        // updates accumulate -C + A B^T (negated once here and once at the store instead of
+        // negating every A fragment)
+        acc[a][b][e] = (UPD && i < na && j < nbv && (!mask || j + doff <= i)) ? -Cb[i + (size_t)j * g.ldc] : 0.0;
       }
   }
 
@@ -394,10 +397,7 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
     for (int k4 = 0; k4 < kBK / 4; ++k4) {
       double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const double v = as[(k4 * 4 + t4) * kLdA + wm * 32 + a * 8 + g8];
-        af[a] = UPD ? neg(v) : v;
-      }
+      for (int a = 0; a < 4; ++a) af[a] = as[(k4 * 4 + t4) * kLdA + wm * 32 + a * 8 + g8];
 #pragma unroll
       for (int b = 0; b < 4; ++b) bf[b] = bs[(k4 * 4 + t4) * kLdB + wn * 32 + b * 8 + g8];
 #pragma unroll
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = wn * 32 + b * 8 + 2 * t4 + e;
-        if (j < nbv && (!mask || j + doff <= i)) Cb[i + (size_t)j * g.ldc] = acc[a][b][e];
+        if (j < nbv && (!mask || j + doff <= i)) Cb[i + (size_t)j * g.ldc] = UPD ? -acc[a][b][e] : acc[a][b][e];
       }
   }
 }
