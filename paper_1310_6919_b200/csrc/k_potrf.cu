@@ -139,63 +139,54 @@ __global__ void __launch_bounds__(kDiagThreads, 1) potrf_diag_kernel(double* B, 
     }
   }
   __syncthreads();
-  // in-kernel lookahead: warp 0 factors the next 32 x 32 diagonal block (after applying the current
-  // panel to it) while warps 1..7 apply the current panel to the rest of the trailing matrix
-  if (wid == 0) {
-    const int f = warp_chol_inv32(A, Dinv[0], lane);
-    if (lane == 0) fail_col = f;
-  }
 #pragma unroll 1
   for (int jb = 0; jb < kNB; jb += 32) {
+    if (wid == 0) {
+      const int f = warp_chol_inv32(A + jb + jb * kLdD, Dinv[jb >> 5], lane);
+      if (lane == 0) fail_col = f;
+    }
     __syncthreads();
     if (fail_col >= 0) {
       if (tid == 0) report_error(err, k0 + jb + fail_col + 1);
       return;
     }
     const int r0 = jb + 32, nr = kNB - r0;
-    if (nr <= 0) break;
-    // P(r, c) = sum_k A(r, jb+k) Linv11(c, k): (nr/8) x 4 tiles of 8 x 8, K = 32
-    const double* Iv = &Dinv[jb >> 5][0][0];
-    const int ntile = (nr / 8) * 4;
-    for (int t = wid; t < ntile; t += kDiagThreads / 32) {
-      const int tr = t >> 2, tc = t & 3;
-      double c0 = 0.0, c1 = 0.0;
-      warp_mma8(c0, c1, A + (r0 + tr * 8) + jb * kLdD, 1, kLdD, Iv + tc * 8 * 33, 33, 1, 32, false, lane);
-      const int r = r0 + tr * 8 + g8, c = tc * 8 + 2 * t4;
-      P[c * kLdD + r] = c0;
-      P[(c + 1) * kLdD + r] = c1;
+    if (nr > 0) {
+      // P(r, c) = sum_k A(r, jb+k) Linv11(c, k): (nr/8) x 4 tiles of 8 x 8, K = 32
+      const double* Iv = &Dinv[jb >> 5][0][0];
+      const int ntile = (nr / 8) * 4;
+      for (int t = wid; t < ntile; t += kDiagThreads / 32) {
+        const int tr = t >> 2, tc = t & 3;
+        double c0 = 0.0, c1 = 0.0;
+        warp_mma8(c0, c1, A + (r0 + tr * 8) + jb * kLdD, 1, kLdD, Iv + tc * 8 * 33, 33, 1, 32, false, lane);
+        const int r = r0 + tr * 8 + g8, c = tc * 8 + 2 * t4;
+        P[c * kLdD + r] = c0;
+        P[(c + 1) * kLdD + r] = c1;
+      }
+      __syncthreads();
+      // panel back into A (its columns are not touched by the update) and the trailing update
+      for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
+        const int c = idx / nr, r = r0 + idx % nr;
+        A[r + (jb + c) * kLdD] = P[c * kLdD + r];
+      }
+      // A22 -= P P^T on the 8 x 8 tiles (ti >= tj) of rows/cols r0..127 (the strict upper part of
+      // the diagonal tiles is scratch: overwritten by L^{-T} below, never read as L)
+      const int nb8 = nr / 8, nt2 = nb8 * (nb8 + 1) / 2;
+      for (int t = wid; t < nt2; t += kDiagThreads / 32) {
+        int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while (ti * (ti + 1) / 2 > t) --ti;
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int i0 = r0 + ti * 8, j0 = r0 + tj * 8;
+        double* Cp = A + (i0 + g8) + (j0 + 2 * t4) * kLdD;
+        double c0 = Cp[0], c1 = Cp[kLdD];
+        warp_mma8(c0, c1, P + i0, 1, kLdD, P + j0, 1, kLdD, 32, true, lane);
+        Cp[0] = c0;
+        Cp[kLdD] = c1;
+      }
     }
     __syncthreads();
-    // panel back into A (its columns are not touched by the update) and the trailing update
-    // A22 -= P P^T on the 8 x 8 tiles (ti >= tj) of rows/cols r0..127, row-major: tiles 0..9 are the
-    // next diagonal block (warp 0, then its factorisation), the rest go to warps 1..7 (the strict
-    // upper part of the diagonal tiles is scratch: overwritten by L^{-T} below, never read as L)
-    for (int idx = tid; idx < nr * 32; idx += kDiagThreads) {
-      const int c = idx / nr, r = r0 + idx % nr;
-      A[r + (jb + c) * kLdD] = P[c * kLdD + r];
-    }
-    const int nb8 = nr / 8, nt2 = nb8 * (nb8 + 1) / 2;
-    const int tfirst = wid == 0 ? 0 : 10 + (wid - 1), tstep = wid == 0 ? 1 : kDiagThreads / 32 - 1;
-    const int tlast = wid == 0 ? 10 : nt2;
-    for (int t = tfirst; t < tlast; t += tstep) {
-      int ti = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-      while (ti * (ti + 1) / 2 > t) --ti;
-      while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-      const int tj = t - ti * (ti + 1) / 2;
-      const int i0 = r0 + ti * 8, j0 = r0 + tj * 8;
-      double* Cp = A + (i0 + g8) + (j0 + 2 * t4) * kLdD;
-      double c0 = Cp[0], c1 = Cp[kLdD];
-      warp_mma8(c0, c1, P + i0, 1, kLdD, P + j0, 1, kLdD, 32, true, lane);
-      Cp[0] = c0;
-      Cp[kLdD] = c1;
-    }
-    if (wid == 0) {
-      __syncwarp();
-      const int f = warp_chol_inv32(A + r0 + r0 * kLdD, Dinv[r0 >> 5], lane);
-      if (lane == 0) fail_col = f;  // checked at the head of the next iteration (jb = r0)
-    }
   }
-  __syncthreads();
   for (int idx = tid; idx < kb * kb; idx += kDiagThreads) {
     const int i = idx % kb, j = idx / kb;
     if (i >= j) Bd[i + (size_t)j * ld] = A[i + j * kLdD];
