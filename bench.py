@@ -172,6 +172,19 @@ def run_ours(args, rank, world, local_rank):
         ms = float(t.item())
         torch.distributed.barrier()
 
+    # NEXT row 2 (not part of the metric): the SCE B dz = g with the factor just computed
+    g_rhs = torch.ones((1, ld), dtype=torch.float64, device=dev)
+    h.scm_solve(Bt, g_rhs, ld, ld, 1, stream)
+    torch.cuda.synchronize()
+    e_s0, e_s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_s0.record(stream)
+    for _ in range(3):
+        g_rhs.fill_(1.0)
+        h.scm_solve(Bt, g_rhs, ld, ld, 1, stream)
+    e_s1.record(stream)
+    e_s1.synchronize()
+    sce_ms = e_s0.elapsed_time(e_s1) / 3
+
     # end to end through the public host-buffer API (H2D inputs + D2H diag(R), info)
     rd = np.zeros(m)
     h.iteration_host(inst.xbar, inst.y, rd)
@@ -224,6 +237,8 @@ def run_ours(args, rank, world, local_rank):
                       "c_accumulate": ph[3], "d_cholesky": ph[4], "d_trailing_updates": upd_ms,
                       "note": "(a1) || (a2) on two streams, each factor's solves start when it is ready"},
         "clocks": clk.summary(),
+        "next_rows": {"sce_solve_ms": sce_ms,
+                      "note": "sdpc_scm_solve (R R^T) dz = g, one RHS, with the factor of the step (not in the metric)"},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
         "roofline": {"kernel": "gemm_nt_kernel<kModeUpdTri> (SCM Cholesky trailing update, K = 256, DMMA)",

@@ -160,6 +160,16 @@ sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t
 sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream);
 
 /*
+ * sdpc_scm_solve - the Schur complement equation (SCE) of the search direction, B dz = g
+ * (SURVEY §8(f) NEXT row 2), with the factor of sdpc_scm_cholesky: (R R^T) X = G.
+ *   R : DEVICE m x m column-major (ldr >= m), lower triangle = R (as left in B by the Cholesky).
+ *   G : DEVICE m x nrhs column-major (ldg >= m), overwritten with X.
+ * Blocked forward / backward substitution (128-row blocks); nranks == 1.
+ */
+sdpc_status sdpc_scm_solve(sdpc_handle h, const double* R, int64_t ldr, double* G, int64_t ldg,
+                           int32_t nrhs, void* stream);
+
+/*
  * Tile entries of the distributed (nranks > 1) SCM Cholesky, a 2D block-cyclic right-looking
  * blocked Cholesky (P:711-713 type (i), P:1012 SDPARA-C's distributed variant).
  * Per step k (tile column k of size kb <= 256, global rows from k1 = 256 k):

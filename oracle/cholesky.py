@@ -20,3 +20,14 @@ def backward_error(B, R):
     Bl = np.tril(B)
     Bs = Bl + np.tril(Bl, -1).T
     return np.linalg.norm(Bs - R @ R.T) / np.linalg.norm(Bs)
+
+
+def sce_solve(B, G):
+    """Solution X of the Schur complement equation B X = G (B dz = g of the HKM
+    search direction), B symmetric positive definite given by its lower triangle.  Plain definition
+    through LAPACK: X = potrs(potrf(B), G).  (SURVEY §8(f) NEXT row 2.)"""
+    import scipy.linalg as sl
+    Bl = np.tril(B)
+    Bs = Bl + np.tril(Bl, -1).T
+    c = sl.cho_factor(Bs, lower=True)
+    return sl.cho_solve(c, np.asarray(G, dtype=np.float64))

@@ -453,7 +453,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
                   h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->ws2, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
-                  h->d_err, h->d_ok, h->pair_ws, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
+                  h->d_err, h->d_ok, h->pair_ws, h->sce_ws, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->pinned_in) cudaFreeHost(h->pinned_in);
@@ -808,6 +808,24 @@ sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const doubl
   CK(cudaSetDevice(h->device));
   h->launches += update_tiles(C, ldc, P, ldp, k1, K, h->grid, h->S.m, h->mloc, h->nloc, h->d_ok,
                               (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_scm_solve(sdpc_handle h, const double* R, int64_t ldr, double* G, int64_t ldg, int32_t nrhs,
+                           void* stream) {
+  if (!h || !R || !G || nrhs < 1 || ldr < h->S.m || ldg < h->S.m) return SDPC_ERR_INVALID_ARG;
+  if (h->nranks != 1) return SDPC_ERR_STATE;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->sce_cap < nrhs) {
+    if (h->sce_ws) cudaFree(h->sce_ws);
+    h->sce_ws = nullptr;
+    CK(dalloc(&h->sce_ws, (size_t)nrhs * 128));
+    h->sce_cap = nrhs;
+  }
+  h->launches += scm_solve(R, ldr, h->S.m, G, ldg, nrhs, h->sce_ws, st);
+  CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
   return SDPC_OK;
 }

@@ -93,6 +93,8 @@ struct sdpc_ctx {
   std::vector<int32_t> slot_of_host;  // host copy of DevSym::slot_of
   std::vector<int32_t> diag_ids;      // host copy of DevCons::dlist
   double* pair_ws = nullptr;          // partial sums of the diagonal-large pair reductions
+  double* sce_ws = nullptr;           // scratch of sdpc_scm_solve (nrhs x 128)
+  int32_t sce_cap = 0;
   int64_t mloc = 0, nloc = 0;      // local rows / columns of B on this rank
   sdpc::Symbolic S;
   sdpc::DevSym d;
@@ -163,5 +165,7 @@ int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t l
 int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1, int K, const Grid& g, int64_t m,
                  int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st);
 int launch_diag_copy(double* B, int64_t m, int64_t ld, double* out, cudaStream_t st);
+// (R R^T) X = G in place, R lower (m x m, ldr); S: nrhs x 128 doubles of scratch
+int scm_solve(const double* R, int64_t ldr, int64_t m, double* G, int64_t ldg, int nrhs, double* S, cudaStream_t st);
 cudaError_t fp64_peak(int device, double ms, double* dmma, double* dfma);
 }  // namespace sdpc

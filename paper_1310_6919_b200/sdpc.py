@@ -29,6 +29,7 @@ _SIGS = [
     ("sdpc_get_y_factor", C.c_int, [_P, _P, _P, _P]),
     ("sdpc_get_inverse_columns", C.c_int, [_P, _P, C.c_int32, _P, _P, _P]),
     ("sdpc_scm_cholesky", C.c_int, [_P, _P, C.c_int64, _P, _P]),
+    ("sdpc_scm_solve", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, _P]),
     ("sdpc_potrf_tile", C.c_int, [_P, _P, C.c_int32, C.c_int64, _P, _P, _P]),
     ("sdpc_trsm_panel", C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_int32, _P]),
     ("sdpc_update_tiles", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int32, _P]),
@@ -168,6 +169,13 @@ class Handle:
             return int(info.value)
         self._check(st, "sdpc_scm_cholesky")
         return int(info.value)
+
+    def scm_solve(self, R, G, ldr=None, ldg=None, nrhs=1, stream=None):
+        """(R R^T) X = G in place (the SCE B dz = g with the SCM factor)."""
+        ldr = self.m if ldr is None else ldr
+        ldg = self.m if ldg is None else ldg
+        self._check(lib().sdpc_scm_solve(self.h, _ptr(R), int(ldr), _ptr(G), int(ldg), int(nrhs), _stream(stream)),
+                    "sdpc_scm_solve")
 
     # -- distributed SCM Cholesky tile entries (asynchronous; see sdpc.h) --
     def potrf_tile(self, A, n, lda, inv, info_dev, stream=None):

@@ -383,3 +383,24 @@ def test_fused_iteration_not_pd_phases():
     with pytest.raises(SdpcError) as e:
         Handle.from_instance(inst).iteration(x, yb, B)
     assert e.value.info == 1
+
+
+@pytest.mark.parametrize("m,nrhs", [(1, 1), (129, 2), (1000, 1), (1311, 3)])
+def test_sce_solve_with_scm_factor(m, nrhs):
+    """NEXT row 2 (SCE): sdpc_scm_solve with the factor of sdpc_scm_cholesky against the
+    oracle's LAPACK solve, ragged sizes and several right-hand sides."""
+    from tests.helpers import scm_handle
+    h = scm_handle(m)
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(m + nrhs)
+    G = rng.standard_normal((m, m + 4))
+    Bh = G @ G.T / (m + 4) + 0.5 * np.eye(m)
+    Bt = torch.from_numpy(np.tril(Bh).T.copy()).to(dev)           # column-major lower
+    assert h.scm_cholesky(Bt, m) == 0
+    Rhs = rng.standard_normal((m, nrhs))
+    Gt = torch.from_numpy(Rhs.T.copy()).to(dev)                    # column-major m x nrhs
+    h.scm_solve(Bt, Gt, m, m, nrhs)
+    X = Gt.cpu().numpy().T
+    Xo = CH.sce_solve(Bh, Rhs)
+    assert rel(X, Xo) < 1e-10
+    assert np.linalg.norm(Bh @ X - Rhs) / np.linalg.norm(Rhs) < 1e-12

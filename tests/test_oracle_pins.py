@@ -335,3 +335,20 @@ def test_algorithm1_not_pd_reports_clique():
     with pytest.raises(A1.NotPositiveDefinite) as e:
         A1.algorithm1(S, x)
     assert e.value.index == 1
+
+
+def test_sce_solve_worked_example_and_residual():
+    """SCE B dz = g: SPEC's 2x2 B = [[4,2],[2,5]] with g = (2, 1) gives
+    dz = B^{-1} g = (1/16)[[5,-2],[-2,4]] (2, 1) = (1/2, 0) exactly; random SPD: residual and
+    multi-RHS = columnwise."""
+    from oracle import cholesky as CHO
+    x = CHO.sce_solve(np.array([[4.0, 2.0], [2.0, 5.0]]), np.array([2.0, 1.0]))
+    np.testing.assert_allclose(x, [0.5, 0.0], atol=1e-15)
+    rng = np.random.default_rng(5)
+    G = rng.standard_normal((60, 70))
+    B = G @ G.T / 70 + np.eye(60)
+    Rhs = rng.standard_normal((60, 3))
+    X = CHO.sce_solve(np.tril(B), Rhs)
+    assert np.linalg.norm(B @ X - Rhs) / np.linalg.norm(Rhs) < 1e-13
+    for q in range(3):
+        np.testing.assert_allclose(CHO.sce_solve(B, Rhs[:, q]), X[:, q], rtol=1e-12, atol=1e-14)
