@@ -424,7 +424,7 @@ def run_reference(args, rank, world):
     last = vals[-1]
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "B-entries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "n": inst.n, "m": inst.m, "seed": args.seed},
             "cpu_baseline": {"value": value, "unit": "B-entries/s", "cores": last["cores"], "kind": "oracle",
                              "sample": last["sample"]},

@@ -194,11 +194,13 @@ sdpc_status sdpc_potrf_tile(sdpc_handle h, double* A, int32_t n, int64_t lda, do
 sdpc_status sdpc_trsm_panel(sdpc_handle h, double* A, int64_t rows, int64_t lda, const double* L,
                             int64_t ldl, const double* inv, int32_t kb, void* stream);
 
-/* sdpc_update_tiles: for every local tile (I, J) of this rank with I >= J and 256 J >= k1:
- * C_IJ -= P_I P_J^T (lower part only when I == J).  C = local array (mloc x nloc, ldc >= mloc);
- * P = the gathered panel: row r is global row k1 + r (r < m - k1), K columns, ldp >= m - k1. */
+/* sdpc_update_tiles: for every local tile (I, J) of this rank with I >= J, 256 J >= k1 and
+ * jlo <= J < jhi (global tile columns; jhi <= 0: no upper bound): C_IJ -= P_I P_J^T (lower part
+ * only when I == J).  C = local array (mloc x nloc, ldc >= mloc); P = the gathered panel: row r is
+ * global row k1 + r (r < m - k1), K columns, ldp >= m - k1.  The column range lets the caller
+ * update the next panel's tile column first (lookahead) and the rest on another stream. */
 sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const double* P, int64_t ldp,
-                              int64_t k1, int32_t K, void* stream);
+                              int64_t k1, int32_t K, int64_t jlo, int64_t jhi, void* stream);
 
 /*
  * sdpc_iteration - the whole hot path on DEVICE buffers in one call (what bench.py times):

@@ -801,13 +801,13 @@ sdpc_status sdpc_trsm_panel(sdpc_handle h, double* A, int64_t rows, int64_t lda,
 }
 
 sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1,
-                              int32_t K, void* stream) {
+                              int32_t K, int64_t jlo, int64_t jhi, void* stream) {
   if (!h || k1 < 0 || K < 1 || K > kScmNB || k1 % kScmNB != 0) return SDPC_ERR_INVALID_ARG;
   if (h->mloc > 0 && h->nloc > 0 && k1 < h->S.m && (!C || !P || ldc < h->mloc || ldp < h->S.m - k1))
     return SDPC_ERR_INVALID_ARG;
   CK(cudaSetDevice(h->device));
   h->launches += update_tiles(C, ldc, P, ldp, k1, K, h->grid, h->S.m, h->mloc, h->nloc, h->d_ok,
-                              (cudaStream_t)stream);
+                              (cudaStream_t)stream, jlo, jhi);
   CK(cudaGetLastError());
   return SDPC_OK;
 }

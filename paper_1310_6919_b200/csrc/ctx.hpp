@@ -163,7 +163,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
 int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t ldl, const double* inv, int kb,
                const int32_t* d_err, cudaStream_t st);
 int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1, int K, const Grid& g, int64_t m,
-                 int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st);
+                 int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st, int64_t jlo, int64_t jhi);
 int launch_diag_copy(double* B, int64_t m, int64_t ld, double* out, cudaStream_t st);
 // (R R^T) X = G in place, R lower (m x m, ldr); S: nrhs x 128 doubles of scratch
 int scm_solve(const double* R, int64_t ldr, int64_t m, double* G, int64_t ldg, int nrhs, double* S, cudaStream_t st);

@@ -254,6 +254,7 @@ struct GemmArgs {
   // is global row k1; local 128-row/column sub-tiles (blockIdx.x, blockIdx.y)
   Grid g;
   int64_t k1, m;
+  int64_t jlo, jhi;  // DIST: global tile columns [jlo, jhi) only (lookahead split)
   const int32_t* err;
 };
 
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
     const int64_t gi = ((la / kScmNB) * g.g.Pr + g.g.pr) * kScmNB + la % kScmNB;
     const int64_t gj = ((lb / kScmNB) * g.g.Pc + g.g.pc) * kScmNB + lb % kScmNB;
     if (gj < g.k1 || gi + kTile <= gj || gi >= g.m) return;
+    if (gj / kScmNB < g.jlo || gj / kScmNB >= g.jhi) return;
     Ab = g.A + (gi - g.k1);
     Bb = g.A + (gj - g.k1);
     Cb = g.C + la + lb * g.ldc;
@@ -732,7 +734,7 @@ int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t l
 // I >= J, J*nb >= k1 gets C_IJ -= P_I P_J^T (lower part of diagonal tiles), P = the gathered panel
 // (global rows k1.. m, K columns).
 int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k1, int K, const Grid& gr, int64_t m,
-                 int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st) {
+                 int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st, int64_t jlo, int64_t jhi) {
   set_all_attrs();
   if (mloc <= 0 || nloc <= 0 || K <= 0 || k1 >= m) return 0;
   GemmArgs g{};
@@ -746,6 +748,8 @@ int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k
   g.g = gr;
   g.k1 = k1;
   g.m = m;
+  g.jlo = jlo;
+  g.jhi = jhi > 0 ? jhi : (int64_t)1 << 40;
   g.err = d_err;
   const bool al16 = aligned16(C, ldc) && aligned16(P, ldp);
   launch_gemm<kModeDist>(al16, dim3((unsigned)((mloc + kTile - 1) / kTile), (unsigned)((nloc + kBN - 1) / kBN)), g,

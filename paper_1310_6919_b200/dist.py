@@ -20,7 +20,8 @@ Cholesky: right-looking blocked, per step k (tile column k):
   3. process column k mod Pc solves its panel tiles (sdpc_trsm_panel);
   4. the panel reaches every rank: broadcast along each process row from column k mod Pc, then
      all-gather within each process column (the transposed operand of the update);
-  5. every rank updates its trailing tiles (sdpc_update_tiles).
+  5. every rank updates its trailing tiles (sdpc_update_tiles): tile column k+1 first, the rest on a
+     side stream while panel k+1 is factored and communicated (depth-1 lookahead).
 """
 from __future__ import annotations
 
@@ -193,8 +194,9 @@ class ThreadComm:
 
 # ----------------------------------------------------------------------------- distributed Cholesky
 
-def update_flops(L: Layout, k: int) -> float:
-    """Algorithmic flops of this rank's trailing update at step k (2 * kb per updated entry)."""
+def update_flops(L: Layout, k: int, jlo: int = 0, jhi: int = 0) -> float:
+    """Algorithmic flops of this rank's trailing update at step k (2 * kb per updated entry),
+    restricted to the global tile columns [jlo, jhi) (jhi <= 0: no bound)."""
     kb = min(NB, L.m - k * NB)
     fl = 0.0
     for I in range(L.myrow, L.nt, L.Pr):
@@ -202,7 +204,7 @@ def update_flops(L: Layout, k: int) -> float:
             continue
         h = L.tile_rows(I)
         for J in range(L.mycol, I + 1, L.Pc):
-            if J <= k:
+            if J <= k or J < jlo or (jhi > 0 and J >= jhi):
                 continue
             w = L.tile_rows(J)
             fl += 2.0 * kb * (h * (h + 1) / 2 if I == J else h * w)
@@ -213,6 +215,10 @@ def dist_cholesky(ops, Bt, L: Layout, comm, dev, stream=None, timer=None):
     """Factor the distributed SCM in place (lower(B) <- R).  Returns the LAPACK-style info (0 or the
     1-based order of the first non-PD leading minor), identical on every rank.
 
+    Depth-1 lookahead: after panel k is on every rank, the tile column k+1 is updated first (on the
+    main stream), panel k+1 is factored, solved and communicated, while the rest of the trailing
+    update of step k runs on a side stream (GPU); panel buffers are double-buffered.
+
     ops: sdpc Handle (GPU) or a test double with the same potrf_tile / trsm_panel / update_tiles.
     Bt:  local array, torch tensor (nloc, lld), local element (r, c) at Bt[c, r].
     timer: optional list; gets (start event, end event, algorithmic flops) per local update launch.
@@ -220,23 +226,29 @@ def dist_cholesky(ops, Bt, L: Layout, comm, dev, stream=None, timer=None):
     import torch
     m, lld = L.m, L.lld
     f64 = torch.float64
+    cuda = dev.type == "cuda"
+    main = torch.cuda.current_stream(dev) if cuda else None
+    side = torch.cuda.Stream(device=dev) if cuda else None
     diagbuf = torch.zeros(NB * NB + INV_ELEMS, dtype=f64, device=dev)
     dtile = diagbuf[:NB * NB].view(NB, NB)        # tile (r, c) at dtile[c, r], ld NB
     dinv = diagbuf[NB * NB:]
     infos = torch.full((L.nt,), NO_ERROR, dtype=torch.int32, device=dev)
     max_tiles = (L.nt + L.Pr - 1) // L.Pr
-    piece = torch.zeros(NB * max_tiles * NB, dtype=f64, device=dev)
-    gathered = [torch.zeros_like(piece) for _ in range(L.Pr)] if L.Pr > 1 else None
-    pfull = torch.zeros(NB * L.nt * NB, dtype=f64, device=dev) if L.Pr > 1 else None
-    for k in range(L.nt):
+    piece = [torch.zeros(NB * max_tiles * NB, dtype=f64, device=dev) for _ in range(2)]
+    gathered = [[torch.zeros_like(piece[0]) for _ in range(L.Pr)] for _ in range(2)] if L.Pr > 1 else None
+    pfull = [torch.zeros(NB * L.nt * NB, dtype=f64, device=dev) for _ in range(2)] if L.Pr > 1 else None
+
+    def panel(k):
+        """Steps 1-4 for tile column k: returns (P, ldp, k1, kb) with P the panel on every rank,
+        or None when k is the last tile column."""
+        buf = k & 1
         k0 = k * NB
         kb = min(NB, m - k0)
         prk, pck = k % L.Pr, k % L.Pc
-        k1 = k0 + kb                                 # first global row of the panel / trailing part
-        mine = L.tiles_after(k, L.myrow)             # my panel tile rows (global tile ids)
+        k1 = k0 + kb
+        mine = L.tiles_after(k, L.myrow)
         r0 = L.local_row_of_tile(mine[0]) if mine else L.mloc
         rows = L.mloc - r0
-        # 1-3: diagonal tile, broadcast down the process column, panel solve
         if L.mycol == pck:
             lc = L.local_col_of_tile(k)
             if L.myrow == prk:
@@ -247,37 +259,60 @@ def dist_cholesky(ops, Bt, L: Layout, comm, dev, stream=None, timer=None):
             if rows > 0:
                 ops.trsm_panel(Bt[lc:, r0:], rows, lld, dtile, NB, dinv, kb, stream)
         if k1 >= m:
-            break
-        # 4: panel to every rank.  piece = my process row's panel tiles, column-major, ld = npr*NB
+            return None
         npr = len(mine)
         ldpc = max(1, npr) * NB
-        pv = piece[:kb * ldpc].view(kb, ldpc)
+        pv = piece[buf][:kb * ldpc].view(kb, ldpc)
         if L.mycol == pck and rows > 0:
             pv[:, :rows].copy_(Bt[L.local_col_of_tile(k):L.local_col_of_tile(k) + kb, r0:L.mloc])
-        comm.bcast_row(piece, pck)
+        comm.bcast_row(piece[buf], pck)
         if L.Pr == 1:
-            P, ldp = pv, ldpc
-        else:
-            comm.allgather_col(gathered, piece)
-            ntr = L.nt - (k + 1)                     # panel tile rows k+1 .. nt-1
-            ldp = ntr * NB
-            P = pfull[:kb * ldp].view(kb, ldp)
-            Pt = P.view(kb, ntr, NB)
-            for pr in range(L.Pr):
-                tl = L.tiles_after(k, pr)
-                if not tl:
-                    continue
-                t0 = tl[0] - (k + 1)
-                src = gathered[pr][:kb * len(tl) * NB].view(kb, len(tl), NB)
-                Pt[:, t0::L.Pr, :].copy_(src)
-        # 5: trailing update of my tiles
+            return pv, ldpc, k1, kb
+        comm.allgather_col(gathered[buf], piece[buf])
+        ntr = L.nt - (k + 1)                     # panel tile rows k+1 .. nt-1
+        ldp = ntr * NB
+        P = pfull[buf][:kb * ldp].view(kb, ldp)
+        Pt = P.view(kb, ntr, NB)
+        for pr in range(L.Pr):
+            tl = L.tiles_after(k, pr)
+            if not tl:
+                continue
+            t0 = tl[0] - (k + 1)
+            src = gathered[buf][pr][:kb * len(tl) * NB].view(kb, len(tl), NB)
+            Pt[:, t0::L.Pr, :].copy_(src)
+        return P, ldp, k1, kb
+
+    def update(P, ldp, k1, kb, k, jlo, jhi, strm):
         if timer is not None:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-        ops.update_tiles(Bt, lld, P, ldp, k1, kb, stream)
+            e0.record(strm)
+        ops.update_tiles(Bt, lld, P, ldp, k1, kb, strm, jlo, jhi)
         if timer is not None:
-            e1.record()
-            timer.append((e0, e1, update_flops(L, k)))
+            e1.record(strm)
+            timer.append((e0, e1, update_flops(L, k, jlo, jhi)))
+
+    cur = panel(0)
+    prev_done = None
+    for k in range(L.nt):
+        if cur is None:
+            break
+        P, ldp, k1, kb = cur
+        # 5a. tile column k+1 first (it holds panel k+1); it needs the bulk update of step k-1
+        if cuda and prev_done is not None:
+            main.wait_event(prev_done)
+        update(P, ldp, k1, kb, k, k + 1, k + 2, main)
+        # 5b. the rest of the trailing update on the side stream, overlapping panel k+1
+        if cuda:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                update(P, ldp, k1, kb, k, k + 2, 0, side)
+            prev_done = torch.cuda.Event()
+            prev_done.record(side)
+        else:
+            update(P, ldp, k1, kb, k, k + 2, 0, None)
+        cur = panel(k + 1)
+    if cuda:
+        main.wait_stream(side)
     # info: smallest failing global column over all ranks (LAPACK rule)
     loc = torch.full((1,), NO_ERROR, dtype=torch.int64, device=dev)
     bad = (infos != NO_ERROR).nonzero().flatten()

@@ -32,7 +32,8 @@ _SIGS = [
     ("sdpc_scm_solve", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, _P]),
     ("sdpc_potrf_tile", C.c_int, [_P, _P, C.c_int32, C.c_int64, _P, _P, _P]),
     ("sdpc_trsm_panel", C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_int32, _P]),
-    ("sdpc_update_tiles", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int32, _P]),
+    ("sdpc_update_tiles", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
+                                    _P]),
     ("sdpc_iteration", C.c_int, [_P, _P, _P, _P, C.c_int64, _P, _P]),
     ("sdpc_iteration_host", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
@@ -186,9 +187,9 @@ class Handle:
         self._check(lib().sdpc_trsm_panel(self.h, _ptr(A), int(rows), int(lda), _ptr(L), int(ldl), _ptr(inv),
                                           int(kb), _stream(stream)), "sdpc_trsm_panel")
 
-    def update_tiles(self, C_loc, ldc, P, ldp, k1, K, stream=None):
+    def update_tiles(self, C_loc, ldc, P, ldp, k1, K, stream=None, jlo=0, jhi=0):
         self._check(lib().sdpc_update_tiles(self.h, _ptr(C_loc), int(ldc), _ptr(P), int(ldp), int(k1), int(K),
-                                            _stream(stream)), "sdpc_update_tiles")
+                                            int(jlo), int(jhi), _stream(stream)), "sdpc_update_tiles")
 
     def iteration(self, xbar_E, y_E, B, ldb=None, stream=None, raise_not_pd=True):
         """(a1) || (a2) -> (b) -> (c) -> (d) on device buffers; returns the Cholesky info."""

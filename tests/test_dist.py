@@ -54,12 +54,12 @@ class CpuTileOps:
         Lm = torch.tril(self._mat(Lt, kb, kb))
         Am.copy_(torch.linalg.solve_triangular(Lm, Am.T, upper=False).T)
 
-    def update_tiles(self, C, ldc, P, ldp, k1, K, stream=None):
+    def update_tiles(self, C, ldc, P, ldp, k1, K, stream=None, jlo=0, jhi=0):
         L = self.L
         Pm = self._mat(P, ldp, K)                    # row r = global row k1 + r
         for I in range(L.myrow, L.nt, L.Pr):
             for J in range(L.mycol, L.nt, L.Pc):
-                if J * D.NB < k1 or I < J:
+                if J * D.NB < k1 or I < J or J < jlo or (jhi > 0 and J >= jhi):
                     continue
                 h, w = L.tile_rows(I), L.tile_rows(J)
                 r, c = L.local_row_of_tile(I), L.local_col_of_tile(J)
