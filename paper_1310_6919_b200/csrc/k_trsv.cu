@@ -28,11 +28,14 @@ constexpr int kTb = 128;
 // products (backward).  2 grid barriers per block instead of 2 dependent launches.
 __device__ __forceinline__ void diag_solve_fwd(const double* __restrict__ R, int64_t ldr, int64_t m, int j0, double* G,
                                                int64_t ldg, int nrhs, double (*Rs)[kTb + 1]) {
+  __shared__ double rd[kTb];
   const int nb = (int)(m - j0 < kTb ? m - j0 : kTb);
   for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
     const int i = idx % nb, c = idx / nb;
     Rs[i][c] = i >= c ? R[(j0 + i) + (size_t)(j0 + c) * ldr] : 0.0;
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) rd[i] = 1.0 / Rs[i][i];  // off the serial chain
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int q = wid; q < nrhs; q += blockDim.x / 32) {
@@ -46,7 +49,7 @@ __device__ __forceinline__ void diag_solve_fwd(const double* __restrict__ R, int
       if (ti == 1) yi = __shfl_sync(0xffffffffu, y[1], li);
       if (ti == 2) yi = __shfl_sync(0xffffffffu, y[2], li);
       if (ti == 3) yi = __shfl_sync(0xffffffffu, y[3], li);
-      yi /= Rs[i][i];
+      yi *= rd[i];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int r = lane + 32 * t;
@@ -71,14 +74,28 @@ __global__ void __launch_bounds__(256) trsv_fwd_coop(const double* __restrict__ 
     if (blockIdx.x == 0) diag_solve_fwd(R, ldr, m, (int)j0, G, ldg, nrhs, Rs);
     grid.sync();
     const int64_t rows = m - j0 - nb;
-    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < rows * nrhs;
-         w += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t r = j0 + nb + w % rows;
-      double* g = G + (size_t)(w / rows) * ldg;
+    // thread = (row, chunk of 16 block columns); the 8 chunks of a row are 8 adjacent lanes
+    const int64_t work = rows * nrhs * 8;
+    for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < work; w0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t w = w0 + threadIdx.x;
+      const int ch = (int)(w & 7);
+      const int64_t rw = w >> 3;
       double acc = 0.0;
-#pragma unroll 8
-      for (int c = 0; c < nb; ++c) acc += R[r + (size_t)(j0 + c) * ldr] * g[j0 + c];
-      g[r] -= acc;
+      int64_t r = 0;
+      double* g = G;
+      if (w < work) {
+        r = j0 + nb + rw % rows;
+        g = G + (size_t)(rw / rows) * ldg;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const int c = ch * 16 + cc;
+          if (c < nb) acc += R[r + (size_t)(j0 + c) * ldr] * g[j0 + c];
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (w < work && ch == 0) g[r] -= acc;
     }
     grid.sync();
   }
@@ -115,10 +132,13 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
       grid.sync();
     }
     if (blockIdx.x == 0) {
+      __shared__ double rdb[kTb];
       for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
         const int i = idx % nb, c = idx / nb;
         Rs[i][c] = i >= c ? R[(j0 + i) + (size_t)(j0 + c) * ldr] : 0.0;
       }
+      __syncthreads();
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) rdb[i] = 1.0 / Rs[i][i];
       __syncthreads();
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
       for (int q = wid; q < nrhs; q += blockDim.x / 32) {
@@ -135,7 +155,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
           if (ti == 1) xi = __shfl_sync(0xffffffffu, v[1], li);
           if (ti == 2) xi = __shfl_sync(0xffffffffu, v[2], li);
           if (ti == 3) xi = __shfl_sync(0xffffffffu, v[3], li);
-          xi /= Rs[i][i];
+          xi *= rdb[i];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int r = lane + 32 * t;
