@@ -12,6 +12,10 @@
  *                      (c)   B_kl = sum_{(p,q) in A_l} [A_l]_pq x_p^T A_k y_q  for k >= l
  *                            (P:380 Eq. SCM; lower triangle only).
  *   sdpc_scm_cholesky  (d)   dense B = R R^T in FP64 (type (i)).
+ *   sdpc_iteration           (a1)..(d) in one call, (a1) || (a2) on two streams, one sync.
+ *   sdpc_scm_solve           the SCE B dz = g with R.
+ *   nranks > 1: sdpc_scm_build writes the rank's 2D block-cyclic tiles; sdpc_potrf_tile,
+ *   sdpc_trsm_panel, sdpc_update_tiles are the tile kernels of the distributed Cholesky (row (e)).
  *
  * Conventions for every entry point:
  *   - 0-based indices.  "E" is the extended sparsity pattern as a lower CSC
