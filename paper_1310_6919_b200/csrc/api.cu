@@ -45,6 +45,7 @@ sdpc_status map_cuda(sdpc_ctx* h, cudaError_t e) {
   } while (0)
 
 constexpr size_t kSmemCap = 200 * 1024;   // dynamic smem per clique CTA (static ~8.5 KB on top)
+constexpr int kSolveCtasDuringA2 = 192;   // ~96 of 148 SMs at 2 solve CTAs per SM
 constexpr size_t kPanelCap = 200 * 1024;  // shared-memory panel of a global-workspace clique
 
 // size classes for the per-clique kernels
@@ -696,7 +697,9 @@ sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_
   CK(cudaStreamWaitEvent(h->st3, h->it_fork, 0));
   h->launches += launch_alg1(h, xbar_E, st);
   if (h->timing) CK(cudaEventRecord(h->ev[1], st));
-  h->launches += launch_inverse_panels(h, st, 0, 1);
+  // cap the X-hat solve grid (each CTA walks several panels) so that about a third of the SMs stay
+  // free for the (a2) levels running concurrently on the high-priority stream
+  h->launches += launch_inverse_panels(h, st, 0, 1, kSolveCtasDuringA2);
   h->launches += launch_ldl_y(h, y_E, h->st3, h->d_err + 1, 1);
   if (h->timing) CK(cudaEventRecord(h->ev[2], h->st3));
   h->launches += launch_inverse_panels(h, h->st3, 1, 1);

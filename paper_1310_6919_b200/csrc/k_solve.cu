@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "ctx.hpp"
 
+#include <algorithm>
+
 namespace sdpc {
 
 struct SolveArgs {
@@ -40,6 +42,7 @@ struct SolveArgs {
   int32_t ntop, nsub;
   int32_t trunc;  // max-cut, one rank: the backward sweep stops below the panel's smallest RHS
   int32_t fac0;   // first factor of this launch (0: X-hat from L, D; 1: Y^{-1} from L_Y, D_Y)
+  int32_t npanels;
   const int32_t* sparent;
   const double* Lp[2];
   const double* D[2];
@@ -350,12 +353,10 @@ __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, 
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
-  extern __shared__ __align__(16) double smem_solve[];
+__device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, const int fac, double* smem_solve) {
   double* Vs = smem_solve;                                                          // chunk of S rows
   double* Bs = smem_solve + kChunk * kVs;                                           // 2 staged K-chunks
   uint32_t* inreach = reinterpret_cast<uint32_t*>(smem_solve + (kChunk + 2 * kKc) * kVs);  // bitmap
-  const int P = blockIdx.x, fac = blockIdx.y + a.fac0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSolveThreads / 32;
   const int n = a.n;
@@ -463,7 +464,18 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   }
 }
 
-int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac) {
+// One CTA per (RHS panel, factor); with gridDim.x < npanels (the X-hat solves that overlap the
+// tree-level (a2) launches leave SMs free for them) each CTA walks panels blockIdx.x + k gridDim.x.
+__global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
+  extern __shared__ __align__(16) double smem_solve[];
+  const int fac = blockIdx.y + a.fac0;
+  for (int P = blockIdx.x; P < a.npanels; P += gridDim.x) {
+    solve_panel(a, P, fac, smem_solve);
+    __syncthreads();
+  }
+}
+
+int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int max_ctas) {
   SolveArgs a{};
   a.n = h->S.n;
   a.nsuper = h->S.nsuper;
@@ -499,7 +511,8 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac) {
   }
   if (h->d.npanels == 0) return 0;
   a.fac0 = fac0;
-  dim3 grid(h->d.npanels, nfac);
+  a.npanels = h->d.npanels;
+  dim3 grid(max_ctas > 0 ? std::min(h->d.npanels, max_ctas) : h->d.npanels, nfac);
   inverse_panel_kernel<<<grid, kSolveThreads, smem, st>>>(a);
   return 1;
 }
