@@ -697,9 +697,11 @@ sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_
   CK(cudaStreamWaitEvent(h->st3, h->it_fork, 0));
   h->launches += launch_alg1(h, xbar_E, st);
   if (h->timing) CK(cudaEventRecord(h->ev[1], st));
-  // cap the X-hat solve grid (each CTA walks several panels) so that about a third of the SMs stay
-  // free for the (a2) levels running concurrently on the high-priority stream
-  h->launches += launch_inverse_panels(h, st, 0, 1, kSolveCtasDuringA2);
+  // deep elimination trees (many (a2) levels, each a latency-bound launch): cap the X-hat solve grid
+  // (each CTA walks several panels) so that about a third of the SMs stay free for the (a2) levels
+  // on the high-priority stream; shallow trees (block-arrow: 2 levels) keep the whole GPU
+  const bool deep = h->a2lev.size() >= 8;
+  h->launches += launch_inverse_panels(h, st, 0, 1, deep ? kSolveCtasDuringA2 : 0);
   h->launches += launch_ldl_y(h, y_E, h->st3, h->d_err + 1, 1);
   if (h->timing) CK(cudaEventRecord(h->ev[2], h->st3));
   h->launches += launch_inverse_panels(h, h->st3, 1, 1);

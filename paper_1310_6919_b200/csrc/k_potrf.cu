@@ -34,6 +34,9 @@ constexpr int kLdB = kBN + 4;
 constexpr int kGemmThreads = 4 * kBN;  // 4 x (kBN/32) warps of 32 x 32
 constexpr int kGemmCtasPerSm = kBN == 64 ? 2 : 1;
 constexpr int kTrsmThreads = 256;  // in-place panel solve: 8 warps x (64 x 32)
+// bulk trailing update on a persistent grid of 2 CTAs x (148 - 6) SMs: 6 SMs stay free for the
+// lookahead stream's panel kernels (one CTA of the diagonal kernel needs a whole SM)
+constexpr int kUpdTriCap = 2 * (148 - 6);
 
 __device__ __forceinline__ double neg(double x) {  // sign flip on the integer pipe
   return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
@@ -255,6 +258,7 @@ struct GemmArgs {
   Grid g;
   int64_t k1, m;
   int64_t jlo, jhi;  // DIST: global tile columns [jlo, jhi) only (lookahead split)
+  int ntiles;        // number of tiles (x-extent); the grid may be smaller (persistent loop)
   const int32_t* err;
 };
 
@@ -262,9 +266,7 @@ enum { kModeTrsm = 0, kModeUpdCols = 1, kModeUpdTri = 2, kModeRect = 3, kModeDis
 
 
 template <int MODE, bool AL16>
-__global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(GemmArgs g) {
-  if (*g.err != kNoError) return;
-  extern __shared__ double sm[];
+__device__ __forceinline__ void gemm_tile(const GemmArgs& g, const int tile, double* sm) {
   double* As = sm;                          // [kStages][kBK][kLdA]
   double* Bs = sm + kStages * kBK * kLdA;   // [kStages][kBK][kLdB]
   constexpr bool UPD = MODE != kModeTrsm;
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
   int na, nbv, doff = 0;
   bool mask;
   if (MODE == kModeTrsm || MODE == kModeRect) {
-    const int bi = blockIdx.x, bj = blockIdx.y;
+    const int bi = tile, bj = blockIdx.y;
     Ab = g.A + (size_t)bi * kTile;
     Bb = g.Bm + (size_t)bj * kBN;
     Cb = g.C + (size_t)bi * kTile + (size_t)bj * kBN * g.ldc;
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
     nbv = g.cols - bj * kBN;
     mask = false;
   } else if (MODE == kModeDist) {
-    const int64_t la = (int64_t)blockIdx.x * kTile, lb = (int64_t)blockIdx.y * kBN;
+    const int64_t la = (int64_t)tile * kTile, lb = (int64_t)blockIdx.y * kBN;
     const int64_t gi = ((la / kScmNB) * g.g.Pr + g.g.pr) * kScmNB + la % kScmNB;
     const int64_t gj = ((lb / kScmNB) * g.g.Pc + g.g.pc) * kScmNB + lb % kScmNB;
     if (gj < g.k1 || gi + kTile <= gj || gi >= g.m) return;
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
     mask = gj + kBN > gi;
   } else {
     const int T = (g.rows + kTile - 1) / kTile;
-    int t = blockIdx.x, bi, bj;  // bj in 64-column units
+    int t = tile, bi, bj;  // bj in 64-column units
     if (MODE == kModeUpdCols) {  // column-major over the 128-columns [c0, c1), two halves each
       int c = g.c0;
       while (t >= kR * (T - c)) {
@@ -424,6 +426,18 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
   }
 }
 
+// Tiles blockIdx.x, blockIdx.x + gridDim.x, ... < g.ntiles (UpdTri may run on a capped, persistent
+// grid so that the panel kernels of the lookahead stream always find free SMs).
+template <int MODE, bool AL16>
+__global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(GemmArgs g) {
+  if (*g.err != kNoError) return;
+  extern __shared__ double sm[];
+  for (int t = blockIdx.x; t < g.ntiles; t += gridDim.x) {
+    gemm_tile<MODE, AL16>(g, t, sm);
+    __syncthreads();  // the next tile's cp.async stages reuse the shared buffers
+  }
+}
+
 // In-place panel solve C = A B^T (C == A allowed: each CTA reads all K columns of its 128 rows
 // before writing any of them, and owns all <= 128 output columns of those rows).  128 x 128 tile,
 // 8 warps x (64 x 32), same pipeline as the update kernel.
@@ -517,8 +531,11 @@ static size_t gemm_smem() { return (size_t)kStages * kBK * (kLdA + kLdB) * sizeo
 static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kLdD + 3 * 32 * 33) * sizeof(double); }  // + 34 KB static
 
 template <int MODE>
-static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g, cudaStream_t st) {
+static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g0, cudaStream_t st, int cap = 0) {
   if (grid.x == 0 || grid.y == 0) return;
+  GemmArgs g = g0;
+  g.ntiles = (int)grid.x;
+  if (cap > 0 && (int)grid.x > cap) grid.x = cap;
   if (MODE == kModeTrsm) {  // in place: one CTA owns all (<= 128) columns of its rows
     if (al16) trsm_kernel<true><<<dim3(grid.x), kTrsmThreads, trsm_smem(), st>>>(g);
     else trsm_kernel<false><<<dim3(grid.x), kTrsmThreads, trsm_smem(), st>>>(g);
@@ -599,7 +616,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     } else {
       const int S = T - c0;
       grid = S > 0 ? kR * S * (S + 1) / 2 : 0;
-      launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s);
+      launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s, kUpdTriCap);
     }
     if (grid > 0) ++launches;
     return grid;
