@@ -34,9 +34,8 @@ constexpr int kLdB = kBN + 4;
 constexpr int kGemmThreads = 4 * kBN;  // 4 x (kBN/32) warps of 32 x 32
 constexpr int kGemmCtasPerSm = kBN == 64 ? 2 : 1;
 constexpr int kTrsmThreads = 256;  // in-place panel solve: 8 warps x (64 x 32)
-// bulk trailing update on a persistent grid of 2 CTAs x (148 - 6) SMs: 6 SMs stay free for the
-// lookahead stream's panel kernels (one CTA of the diagonal kernel needs a whole SM)
-constexpr int kUpdTriCap = 2 * (148 - 6);
+// (a persistent bulk-update grid leaving 6 SMs free for the lookahead stream was measured slower:
+// 19.3 vs 17.5 ms on configs[1]; the update launches one CTA per tile)
 
 __device__ __forceinline__ double neg(double x) {  // sign flip on the integer pipe
   return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
@@ -616,7 +615,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     } else {
       const int S = T - c0;
       grid = S > 0 ? kR * S * (S + 1) / 2 : 0;
-      launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s, kUpdTriCap);
+      launch_gemm<kModeUpdTri>(al16, dim3(grid), u, s);
     }
     if (grid > 0) ++launches;
     return grid;
