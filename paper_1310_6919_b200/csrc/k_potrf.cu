@@ -535,19 +535,19 @@ static void launch_gemm(bool al16, dim3 grid, const GemmArgs& g0, cudaStream_t s
   GemmArgs g = g0;
   g.ntiles = (int)grid.x;
   if (cap > 0 && (int)grid.x > cap) grid.x = cap;
-  if (MODE == kModeTrsm) {  // in place: one CTA owns all (<= 128) columns of its rows
+  if constexpr (MODE == kModeTrsm) {  // in place: one CTA owns all (<= 128) columns of its rows
     if (al16) trsm_kernel<true><<<dim3(grid.x), kTrsmThreads, trsm_smem(), st>>>(g);
     else trsm_kernel<false><<<dim3(grid.x), kTrsmThreads, trsm_smem(), st>>>(g);
-    return;
+  } else {
+    if (al16) gemm_nt_kernel<MODE, true><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
+    else gemm_nt_kernel<MODE, false><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
   }
-  if (al16) gemm_nt_kernel<MODE, true><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
-  else gemm_nt_kernel<MODE, false><<<grid, kGemmThreads, gemm_smem(), st>>>(g);
 }
 
 static void set_all_attrs();
 
 template <int MODE>
-static void set_gemm_attr() {
+static void set_gemm_attr() {  // (never for kModeTrsm: that mode launches trsm_kernel)
   cudaFuncSetAttribute(gemm_nt_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
   cudaFuncSetAttribute(gemm_nt_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem());
 }
