@@ -33,7 +33,7 @@ constexpr int kLdA = kTile + 4;   // smem row strides (doubles): conflict-free f
 constexpr int kLdB = kBN + 4;
 constexpr int kGemmThreads = 4 * kBN;  // 4 x (kBN/32) warps of 32 x 32
 constexpr int kGemmCtasPerSm = kBN == 64 ? 2 : 1;
-constexpr int kTrsmThreads = 256;  // in-place panel solve: 8 warps x (64 x 32)
+constexpr int kTrsmThreads = 256;  // in-place panel solve: 8 warps x (32 x 32)
 // (a persistent bulk-update grid leaving 6 SMs free for the lookahead stream was measured slower:
 // 19.3 vs 17.5 ms on configs[1]; the update launches one CTA per tile)
 
@@ -437,41 +437,42 @@ __global__ void __launch_bounds__(kGemmThreads, kGemmCtasPerSm) gemm_nt_kernel(G
   }
 }
 
-// In-place panel solve C = A B^T (C == A allowed: each CTA reads all K columns of its 128 rows
-// before writing any of them, and owns all <= 128 output columns of those rows).  128 x 128 tile,
-// 8 warps x (64 x 32), same pipeline as the update kernel.
+// In-place panel solve C = A B^T (C == A allowed: each CTA reads all K columns of its rows before
+// writing any of them, and owns all <= 128 output columns of those rows).  64-row x 128-column tile,
+// 8 warps x (32 x 32) DMMA, 2 CTAs per SM (twice the CTAs of a 128-row tile on the critical path).
+constexpr int kTrsmBM = 64;
+constexpr int kLdT = kTrsmBM + 4;
 template <bool AL16>
-__global__ void __launch_bounds__(kTrsmThreads, 1) trsm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kTrsmThreads, 2) trsm_kernel(GemmArgs g) {
   if (*g.err != kNoError) return;
   extern __shared__ double sm[];
-  double* As = sm;                          // [kStages][kBK][kLdA]
-  double* Bs = sm + kStages * kBK * kLdA;   // [kStages][kBK][kLdA]
+  double* As = sm;                          // [kStages][kBK][kLdT]
+  double* Bs = sm + kStages * kBK * kLdT;   // [kStages][kBK][kLdA]
   const int bi = blockIdx.x;
-  const double* Ab = g.A + (size_t)bi * kTile;
-  double* Cb = g.C + (size_t)bi * kTile;
-  const int na = g.rows - bi * kTile, nbv = g.cols;
+  const double* Ab = g.A + (size_t)bi * kTrsmBM;
+  double* Cb = g.C + (size_t)bi * kTrsmBM;
+  const int na = g.rows - bi * kTrsmBM, nbv = g.cols;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int wm = wid >> 2, wn = wid & 3;
+  const int wm = wid >> 2, wn = wid & 3;  // 2 x 4 warps, warp tile 32 x 32
   const int g8 = lane >> 2, t4 = lane & 3;
   auto load_stage = [&](int stage, int k0) {
-    double* as = As + stage * kBK * kLdA;
+    double* as = As + stage * kBK * kLdT;
     double* bs = Bs + stage * kBK * kLdA;
+#pragma unroll
+    for (int q = 0; q < (kBK * kTrsmBM) / kTrsmThreads; ++q) {
+      const int cid = tid + q * kTrsmThreads;
+      const int kk = cid / kTrsmBM, rp = cid % kTrsmBM;
+      const bool va = (k0 + kk) < g.K && rp < na;
+      cp_async8(as + kk * kLdT + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
+    }
 #pragma unroll
     for (int q = 0; q < (kBK * kTile) / kTrsmThreads; ++q) {
       const int cid = tid + q * kTrsmThreads;
       const int kk = cid / kTile, rp = cid % kTile;
-      const bool kv = (k0 + kk) < g.K;
+      const bool vb = (k0 + kk) < g.K && rp < nbv;
       if (AL16) {
-        if ((rp & 1) == 0) {
-          const bool va = kv && rp < na;
-          cp_async16(as + kk * kLdA + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
-          const bool vb = kv && rp < nbv;
-          cp_async16(bs + kk * kLdA + rp, vb ? g.Bm + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
-        }
+        if ((rp & 1) == 0) cp_async16(bs + kk * kLdA + rp, vb ? g.Bm + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
       } else {
-        const bool va = kv && rp < na;
-        cp_async8(as + kk * kLdA + rp, va ? Ab + rp + (size_t)(k0 + kk) * g.lda : g.A, va);
-        const bool vb = kv && rp < nbv;
         cp_async8(bs + kk * kLdA + rp, vb ? g.Bm + rp + (size_t)(k0 + kk) * g.ldbm : g.A, vb);
       }
     }
@@ -482,9 +483,9 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_kernel(GemmArgs g) {
     if (s < nk) load_stage(s, s * kBK);
     cp_async_commit();
   }
-  double acc[8][4][2];
+  double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   for (int kc = 0; kc < nk; ++kc) {
@@ -493,17 +494,17 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_kernel(GemmArgs g) {
     const int nxt = kc + kStages - 1;
     if (nxt < nk) load_stage(nxt % kStages, nxt * kBK);
     cp_async_commit();
-    const double* as = As + (kc % kStages) * kBK * kLdA;
+    const double* as = As + (kc % kStages) * kBK * kLdT;
     const double* bs = Bs + (kc % kStages) * kBK * kLdA;
 #pragma unroll
     for (int k4 = 0; k4 < kBK / 4; ++k4) {
-      double af[8], bf[4];
+      double af[4], bf[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) af[a] = as[(k4 * 4 + t4) * kLdA + wm * 64 + a * 8 + g8];
+      for (int a = 0; a < 4; ++a) af[a] = as[(k4 * 4 + t4) * kLdT + wm * 32 + a * 8 + g8];
 #pragma unroll
       for (int b = 0; b < 4; ++b) bf[b] = bs[(k4 * 4 + t4) * kLdA + wn * 32 + b * 8 + g8];
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
@@ -511,8 +512,8 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_kernel(GemmArgs g) {
   cp_async_wait<0>();
   __syncthreads();  // every warp of this CTA has read its A rows before any is overwritten
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int i = wm * 64 + a * 8 + g8;
+  for (int a = 0; a < 4; ++a) {
+    const int i = wm * 32 + a * 8 + g8;
     if (i >= na) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b)
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_kernel(GemmArgs g) {
   }
 }
 
-static size_t trsm_smem() { return (size_t)2 * kStages * kBK * kLdA * sizeof(double); }
+static size_t trsm_smem() { return (size_t)kStages * kBK * (kLdT + kLdA) * sizeof(double); }
 
 static size_t gemm_smem() { return (size_t)kStages * kBK * (kLdA + kLdB) * sizeof(double); }
 static size_t diag_smem() { return ((size_t)kNB * kLdD + 32 * kLdD + 3 * 32 * 33) * sizeof(double); }  // + 34 KB static
@@ -638,7 +639,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     g.cols = kb;
     g.K = kb;
     g.err = d_err;
-    launch_gemm<kModeTrsm>(al16, dim3((rows + kTile - 1) / kTile), g, s);
+    launch_gemm<kModeTrsm>(al16, dim3((rows + kTrsmBM - 1) / kTrsmBM), g, s);
     ++launches;
   };
   auto panel = [&](int64_t k0, cudaStream_t s) {  // outer block column [k0, k0 + w)
@@ -724,7 +725,8 @@ int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t l
   g.cols = std::min(kb, kNB);
   g.K = g.cols;
   g.err = d_err;
-  launch_gemm<kModeTrsm>(al16, gr, g, st);
+  const dim3 gt((unsigned)((rows + kTrsmBM - 1) / kTrsmBM));
+  launch_gemm<kModeTrsm>(al16, gt, g, st);
   ++launches;
   if (kb > kNB) {
     GemmArgs r = g;
@@ -740,7 +742,7 @@ int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t l
     t.Bm = inv + kNB * kNB;
     t.cols = kb - kNB;
     t.K = kb - kNB;
-    launch_gemm<kModeTrsm>(al16, gr, t, st);
+    launch_gemm<kModeTrsm>(al16, gt, t, st);
     launches += 2;
   }
   return launches;
