@@ -26,14 +26,24 @@ constexpr int kTb = 128;
 // block, CTA 0 solves the diagonal triangle while the others wait at a grid barrier, then every CTA
 // applies the block to its share of the remaining rows (forward) / reduces its share of the dot
 // products (backward).  2 grid barriers per block instead of 2 dependent launches.
+// Stage the lower triangle of the diagonal block [j0, j0+nb)^2 of R into Rs (upper part zero-filled)
+// with cp.async: all loads in flight at once, and issued one block ahead (R is read-only during the
+// solve), so the serial triangle solve never waits on DRAM latency.
+__device__ __forceinline__ void prefetch_tri(const double* __restrict__ R, int64_t ldr, int64_t m, int64_t j0,
+                                             double (*Rs)[kTb + 1]) {
+  const int nb = (int)(m - j0 < kTb ? m - j0 : kTb);
+  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+    const int i = idx % nb, c = idx / nb;
+    cp_async8(&Rs[i][c], i >= c ? R + (j0 + i) + (size_t)(j0 + c) * ldr : R, i >= c);
+  }
+  cp_async_commit();
+}
+
 __device__ __forceinline__ void diag_solve_fwd(const double* __restrict__ R, int64_t ldr, int64_t m, int j0, double* G,
                                                int64_t ldg, int nrhs, double (*Rs)[kTb + 1]) {
   __shared__ double rd[kTb];
   const int nb = (int)(m - j0 < kTb ? m - j0 : kTb);
-  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-    const int i = idx % nb, c = idx / nb;
-    Rs[i][c] = i >= c ? R[(j0 + i) + (size_t)(j0 + c) * ldr] : 0.0;
-  }
+  cp_async_wait<0>();
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x) rd[i] = 1.0 / Rs[i][i];  // off the serial chain
   __syncthreads();
@@ -69,9 +79,13 @@ __global__ void __launch_bounds__(256) trsv_fwd_coop(const double* __restrict__ 
   extern __shared__ double trsv_sm[];
   double (*Rs)[kTb + 1] = reinterpret_cast<double (*)[kTb + 1]>(trsv_sm);
   cg::grid_group grid = cg::this_grid();
+  if (blockIdx.x == 0 && m > 0) prefetch_tri(R, ldr, m, 0, Rs);
   for (int64_t j0 = 0; j0 < m; j0 += kTb) {
     const int nb = (int)(m - j0 < kTb ? m - j0 : kTb);
-    if (blockIdx.x == 0) diag_solve_fwd(R, ldr, m, (int)j0, G, ldg, nrhs, Rs);
+    if (blockIdx.x == 0) {
+      diag_solve_fwd(R, ldr, m, (int)j0, G, ldg, nrhs, Rs);
+      if (j0 + kTb < m) prefetch_tri(R, ldr, m, j0 + kTb, Rs);  // overlaps the update phase
+    }
     grid.sync();
     const int64_t rows = m - j0 - nb;
     // thread = (row, chunk of 16 block columns); the 8 chunks of a row are 8 adjacent lanes
@@ -108,6 +122,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
   __shared__ double red[8];
   cg::grid_group grid = cg::this_grid();
   const int64_t nblk = (m + kTb - 1) / kTb;
+  if (blockIdx.x == 0 && nblk > 0) prefetch_tri(R, ldr, m, (nblk - 1) * kTb, Rs);
   for (int64_t jb = nblk - 1; jb >= 0; --jb) {
     const int64_t j0 = jb * kTb;
     const int nb = (int)(m - j0 < kTb ? m - j0 : kTb);
@@ -117,8 +132,16 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
         const int c = task % nb, q = task / nb;
         const double* col = R + (size_t)(j0 + c) * ldr;
         const double* x = X + (size_t)q * ldx;
-        double acc = 0.0;
-        for (int64_t r = j0 + nb + threadIdx.x; r < m; r += blockDim.x) acc += col[r] * x[r];
+        double acc = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;  // 4 independent chains: loads in flight
+        int64_t r = j0 + nb + threadIdx.x;
+        for (; r + 3 * blockDim.x < m; r += 4 * blockDim.x) {
+          acc += col[r] * x[r];
+          acc1 += col[r + blockDim.x] * x[r + blockDim.x];
+          acc2 += col[r + 2 * blockDim.x] * x[r + 2 * blockDim.x];
+          acc3 += col[r + 3 * blockDim.x] * x[r + 3 * blockDim.x];
+        }
+        for (; r < m; r += blockDim.x) acc += col[r] * x[r];
+        acc += (acc1 + acc2) + acc3;
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
         __syncthreads();
@@ -133,10 +156,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
     }
     if (blockIdx.x == 0) {
       __shared__ double rdb[kTb];
-      for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-        const int i = idx % nb, c = idx / nb;
-        Rs[i][c] = i >= c ? R[(j0 + i) + (size_t)(j0 + c) * ldr] : 0.0;
-      }
+      cp_async_wait<0>();
       __syncthreads();
       for (int i = threadIdx.x; i < nb; i += blockDim.x) rdb[i] = 1.0 / Rs[i][i];
       __syncthreads();
@@ -168,6 +188,7 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
           if (lane + 32 * t < nb) x[lane + 32 * t] = v[t];
       }
       __syncthreads();
+      if (jb > 0) prefetch_tri(R, ldr, m, (jb - 1) * kTb, Rs);  // overlaps the next reduction phase
     }
     grid.sync();
   }
