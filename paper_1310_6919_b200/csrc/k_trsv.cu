@@ -47,31 +47,33 @@ __device__ __forceinline__ void diag_solve_fwd(const double* __restrict__ R, int
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x) rd[i] = 1.0 / Rs[i][i];  // off the serial chain
   __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int q = wid; q < nrhs; q += blockDim.x / 32) {
-    double* g = G + (size_t)q * ldg + j0;
-    double y[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) y[t] = (lane + 32 * t < nb) ? g[lane + 32 * t] : 0.0;
-    for (int i = 0; i < nb; ++i) {
-      const int ti = i >> 5, li = i & 31;
-      double yi = __shfl_sync(0xffffffffu, y[0], li);
-      if (ti == 1) yi = __shfl_sync(0xffffffffu, y[1], li);
-      if (ti == 2) yi = __shfl_sync(0xffffffffu, y[2], li);
-      if (ti == 3) yi = __shfl_sync(0xffffffffu, y[3], li);
-      yi *= rd[i];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int r = lane + 32 * t;
-        if (r == i) y[t] = yi;
-        else if (r > i && r < nb) y[t] -= Rs[r][i] * yi;
+  // 32-row sub-blocks: a warp per RHS solves the 32-triangle (lane = row, one shuffle per step),
+  // then the CTA applies it to the rows below (thread per (row, RHS)); short serial chains only
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int s0 = 0; s0 < nb; s0 += 32) {
+    const int sb = nb - s0 < 32 ? nb - s0 : 32;
+    for (int q = wid; q < nrhs; q += nw) {
+      double* g = G + (size_t)q * ldg + j0 + s0;
+      double y = lane < sb ? g[lane] : 0.0;
+      for (int i = 0; i < sb; ++i) {
+        const double yi = __shfl_sync(0xffffffffu, y, i) * rd[s0 + i];
+        if (lane == i) y = yi;
+        else if (lane > i && lane < sb) y -= Rs[s0 + lane][s0 + i] * yi;
       }
+      if (lane < sb) g[lane] = y;
     }
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (lane + 32 * t < nb) g[lane + 32 * t] = y[t];
+    __syncthreads();
+    const int rem = nb - s0 - sb;
+    for (int idx = threadIdx.x; idx < rem * nrhs; idx += blockDim.x) {
+      const int r = s0 + sb + idx % rem, q = idx / rem;
+      double* g = G + (size_t)q * ldg + j0;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < sb; ++c) acc += Rs[r][s0 + c] * g[s0 + c];
+      g[r] -= acc;
+    }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) trsv_fwd_coop(const double* __restrict__ R, int64_t ldr, int64_t m, double* G,
@@ -160,34 +162,39 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
       __syncthreads();
       for (int i = threadIdx.x; i < nb; i += blockDim.x) rdb[i] = 1.0 / Rs[i][i];
       __syncthreads();
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-      for (int q = wid; q < nrhs; q += blockDim.x / 32) {
-        double* x = X + (size_t)q * ldx + j0;
-        double v[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int r = lane + 32 * t;
-          v[t] = r < nb ? x[r] - (has_s ? S[(size_t)q * kTb + r] : 0.0) : 0.0;
+      if (has_s) {
+        for (int idx = threadIdx.x; idx < nb * nrhs; idx += blockDim.x) {
+          const int r = idx % nb, q = idx / nb;
+          X[(size_t)q * ldx + j0 + r] -= S[(size_t)q * kTb + r];
         }
-        for (int i = nb - 1; i >= 0; --i) {
-          const int ti = i >> 5, li = i & 31;
-          double xi = __shfl_sync(0xffffffffu, v[0], li);
-          if (ti == 1) xi = __shfl_sync(0xffffffffu, v[1], li);
-          if (ti == 2) xi = __shfl_sync(0xffffffffu, v[2], li);
-          if (ti == 3) xi = __shfl_sync(0xffffffffu, v[3], li);
-          xi *= rdb[i];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int r = lane + 32 * t;
-            if (r == i) v[t] = xi;
-            else if (r < i) v[t] -= Rs[i][r] * xi;
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (lane + 32 * t < nb) x[lane + 32 * t] = v[t];
+        __syncthreads();
       }
-      __syncthreads();
+      // 32-row sub-blocks from the last: warp per RHS on the transposed 32-triangle, then the CTA
+      // applies it to the rows above
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int s0 = ((nb - 1) / 32) * 32; s0 >= 0; s0 -= 32) {
+        const int sb = nb - s0 < 32 ? nb - s0 : 32;
+        for (int q = wid; q < nrhs; q += nw) {
+          double* x = X + (size_t)q * ldx + j0 + s0;
+          double v = lane < sb ? x[lane] : 0.0;
+          for (int i = sb - 1; i >= 0; --i) {
+            const double xi = __shfl_sync(0xffffffffu, v, i) * rdb[s0 + i];
+            if (lane == i) v = xi;
+            else if (lane < i) v -= Rs[s0 + i][s0 + lane] * xi;
+          }
+          if (lane < sb) x[lane] = v;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < s0 * nrhs; idx += blockDim.x) {
+          const int r = idx % s0, q = idx / s0;
+          double* x = X + (size_t)q * ldx + j0;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < sb; ++c) acc += Rs[s0 + c][r] * x[s0 + c];
+          x[r] -= acc;
+        }
+        __syncthreads();
+      }
       if (jb > 0) prefetch_tri(R, ldr, m, (jb - 1) * kTb, Rs);  // overlaps the next reduction phase
     }
     grid.sync();
