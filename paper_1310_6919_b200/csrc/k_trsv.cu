@@ -2,12 +2,13 @@
 // (the SCE  B dz = g  of the HKM direction, solved with
 // the factor of type (i)).  R is the lower factor left in B by sdpc_scm_cholesky.
 //
-// Blocked by kTb = 128 rows.  Forward (R Y = G): for each block j, one CTA solves the diagonal
-// triangle for all right-hand sides (warp per RHS, lanes over rows of the 32-row sub-blocks), then a
-// grid-wide update G[below] -= R[below, j] Y_j (thread per row, coalesced reads of the column panel).
-// Backward (R^T X = Y): for each block j from the last, a grid-wide reduction S_j = R[below, j]^T X
-// (CTA per column of the block) then the transposed triangle.  The factor is read once per sweep (the
-// solve is HBM-bound: m^2/2 doubles per sweep); each sweep is one cooperative launch.
+// Blocked by kTb = 128 rows, both sweeps right-looking.  Forward (R Y = G): for each block j, one CTA
+// solves the diagonal triangle for all right-hand sides (32-row sub-triangles, warp per RHS, lane =
+// row), then a grid-wide update G[below] -= R[below, j] Y_j (8 lanes per row split the 128 columns).
+// Backward (R^T X = Y): for each block j from the last, the transposed triangle, then a grid-wide
+// update X[above] -= R[j, above]^T X_j (8 lanes per row of R^T read contiguous runs of a column of
+// R).  The factor is read once per sweep (HBM-bound: m^2/2 doubles per sweep); each sweep is one
+// cooperative launch, the next diagonal triangle is prefetched (cp.async) during the update phase.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -118,57 +119,21 @@ __global__ void __launch_bounds__(256) trsv_fwd_coop(const double* __restrict__ 
 }
 
 __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ R, int64_t ldr, int64_t m, double* X,
-                                                     int64_t ldx, int nrhs, double* S) {
+                                                     int64_t ldx, int nrhs, double* /*S: unused*/) {
   extern __shared__ double trsv_sm[];
   double (*Rs)[kTb + 1] = reinterpret_cast<double (*)[kTb + 1]>(trsv_sm);
-  __shared__ double red[8];
   cg::grid_group grid = cg::this_grid();
   const int64_t nblk = (m + kTb - 1) / kTb;
   if (blockIdx.x == 0 && nblk > 0) prefetch_tri(R, ldr, m, (nblk - 1) * kTb, Rs);
   for (int64_t jb = nblk - 1; jb >= 0; --jb) {
     const int64_t j0 = jb * kTb;
     const int nb = (int)(m - j0 < kTb ? m - j0 : kTb);
-    const bool has_s = j0 + nb < m;
-    if (has_s) {  // S[q][c] = sum_{r >= j0+nb} R[r, j0+c] X[r]: CTA per (column, RHS) task
-      for (int task = blockIdx.x; task < nb * nrhs; task += gridDim.x) {
-        const int c = task % nb, q = task / nb;
-        const double* col = R + (size_t)(j0 + c) * ldr;
-        const double* x = X + (size_t)q * ldx;
-        double acc = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;  // 4 independent chains: loads in flight
-        int64_t r = j0 + nb + threadIdx.x;
-        for (; r + 3 * blockDim.x < m; r += 4 * blockDim.x) {
-          acc += col[r] * x[r];
-          acc1 += col[r + blockDim.x] * x[r + blockDim.x];
-          acc2 += col[r + 2 * blockDim.x] * x[r + 2 * blockDim.x];
-          acc3 += col[r + 3 * blockDim.x] * x[r + 3 * blockDim.x];
-        }
-        for (; r < m; r += blockDim.x) acc += col[r] * x[r];
-        acc += (acc1 + acc2) + acc3;
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          double s = 0.0;
-          for (int w = 0; w < 8; ++w) s += red[w];
-          S[(size_t)q * kTb + c] = s;
-        }
-        __syncthreads();
-      }
-      grid.sync();
-    }
     if (blockIdx.x == 0) {
       __shared__ double rdb[kTb];
       cp_async_wait<0>();
       __syncthreads();
       for (int i = threadIdx.x; i < nb; i += blockDim.x) rdb[i] = 1.0 / Rs[i][i];
       __syncthreads();
-      if (has_s) {
-        for (int idx = threadIdx.x; idx < nb * nrhs; idx += blockDim.x) {
-          const int r = idx % nb, q = idx / nb;
-          X[(size_t)q * ldx + j0 + r] -= S[(size_t)q * kTb + r];
-        }
-        __syncthreads();
-      }
       // 32-row sub-blocks from the last: warp per RHS on the transposed 32-triangle, then the CTA
       // applies it to the rows above
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -195,7 +160,34 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
         }
         __syncthreads();
       }
-      if (jb > 0) prefetch_tri(R, ldr, m, (jb - 1) * kTb, Rs);  // overlaps the next reduction phase
+      if (jb > 0) prefetch_tri(R, ldr, m, (jb - 1) * kTb, Rs);  // overlaps the update phase
+    }
+    grid.sync();
+    // right-looking transposed update of the rows above: X[r] -= sum_c R[j0+c, r] X[j0+c], r < j0.
+    // Row j0+c of R restricted to column r is contiguous in c (column-major), so the 8 lanes of a row
+    // read interleaved, coalesced 64-B runs of column r
+    const int64_t work = j0 * nrhs * 8;
+    for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x; w0 < work; w0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t w = w0 + threadIdx.x;
+      const int ch = (int)(w & 7);
+      const int64_t rw = w >> 3;
+      double acc = 0.0;
+      int64_t r = 0;
+      double* x = X;
+      if (w < work) {
+        r = rw % j0;
+        x = X + (size_t)(rw / j0) * ldx;
+        const double* col = R + (size_t)r * ldr + j0;
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const int c = ch + 8 * cc;
+          if (c < nb) acc += col[c] * x[j0 + c];
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (w < work && ch == 0) x[r] -= acc;
     }
     grid.sync();
   }
