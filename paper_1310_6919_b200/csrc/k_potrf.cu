@@ -27,8 +27,8 @@ constexpr int kNB = 128;         // panel width
 constexpr int kTile = 128;        // GEMM tile rows (BM); also the row/column unit of the tile grids
 constexpr int kBN = 64;           // GEMM tile columns (64: 2 CTAs/SM of 8 warps; 128: 1 CTA/SM of 16 warps)
 constexpr int kR = kTile / kBN;   // GEMM column tiles per 128-column unit
-constexpr int kBK = 32;           // k-chunk per pipeline stage (8 DMMA k-steps per barrier)
-constexpr int kStages = 2;
+constexpr int kBK = 16;           // k-chunk per pipeline stage (4 DMMA k-steps per barrier)
+constexpr int kStages = 4;
 constexpr int kLdA = kTile + 4;   // smem row strides (doubles): conflict-free fragment loads
 constexpr int kLdB = kBN + 4;
 constexpr int kWM = 32;           // update-GEMM warp tile rows (warp tile kWM x 32; 64 x 32 with 4 warps
