@@ -148,6 +148,25 @@ sdpc_status sdpc_get_y_factor(sdpc_handle h, double* LY_E, double* DY, void* str
 sdpc_status sdpc_set_truncation(sdpc_handle h, int32_t on);
 
 /*
+ * Schedule of the one-GPU SCM Cholesky (d).  1 (default): one persistent kernel over the
+ * tile task graph (128-tiles; POTRF / TRSM / trailing-update tasks popped from device ready queues as
+ * their inputs complete); used when B is 16-byte aligned with an even ldb, else 0 is used.  0: the
+ * multi-launch blocked schedule with depth-2 lookahead on two streams.  Same result up to rounding.
+ */
+sdpc_status sdpc_set_cholesky_schedule(sdpc_handle h, int32_t task_graph);
+
+/*
+ * Diagnostics of the task-graph Cholesky: with cap > 0 every later factorisation records up to cap
+ * tasks as {task word, start ns, end ns, smid | cta << 32} (GPU global timer; task word = type << 60 |
+ * half << 56 | k << 32 | i << 16 | j, type 1 POTRF, 2 TRSM, 3 UPD); cap = 0 turns it off.
+ * sdpc_get_cholesky_trace copies the trace buffer (HOST out [4 cap]) and the record count; when
+ * cap >= 1 + 4T (T = ceil(m / 128)) its last 16T words hold per-POTRF phase stamps [T][16] (start, tile
+ * loaded, 4 x panel factored, L stored, end, inverse computed, 6 x inverse block done).
+ */
+sdpc_status sdpc_set_cholesky_trace(sdpc_handle h, int64_t cap);
+sdpc_status sdpc_get_cholesky_trace(sdpc_handle h, uint64_t* out, int64_t cap, int64_t* n);
+
+/*
  * Copy selected columns of X-hat and Y^{-1} computed by the last sdpc_scm_build ((b) output,
  * for verification; STATE if that build used the truncated sweep).  cols: HOST [ncols] ORIGINAL vertex ids.  X_out, Y_out: DEVICE
  * n x ncols column-major (ld = n), rows in ORIGINAL order.

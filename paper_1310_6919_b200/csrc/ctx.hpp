@@ -125,6 +125,15 @@ struct sdpc_ctx {
   double* pinned_in = nullptr;   // pinned host staging (2*nnzE)
   double* pinned_out = nullptr;  // pinned host staging (m)
   double* potrf_ws = nullptr;    // inverses of the diagonal blocks (2 x nb x nb, double-buffered)
+  // persistent task-graph Cholesky (k_chol_dag.cu): zeroed control/counters/queues, L_kk^{-1} tiles
+  void* dag_ws = nullptr;
+  double* dag_linv = nullptr;
+  int64_t* dag_koff = nullptr;
+  int dag_T = -1, dag_dev = -1, dag_grid = 0;
+  bool use_dag = true;           // sdpc_set_cholesky_schedule: 1 = task graph, 0 = round-1 multi-launch
+  size_t dag_zero_bytes = 0;
+  unsigned long long* dag_trace = nullptr;  // optional per-task trace (sdpc_set_cholesky_trace)
+  int64_t dag_trace_cap = 0;
   cudaStream_t st2 = nullptr;    // lookahead stream of the SCM Cholesky
   cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // = sides[0]: (a1) size classes
   cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -159,6 +168,10 @@ int launch_gather_columns(sdpc_ctx* h, const int32_t* d_cols_new, int32_t ncols,
 // (1-based failing column, kNoError if ok).  If upd_times, records an event pair per trailing update.
 int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st, double* flops_upd,
                 int* n_upd, double* linv_ws);
+// The same factorisation as one persistent kernel over the tile task graph (k_chol_dag.cu); needs B
+// 16-byte aligned with an even ld (potrf_dag_usable).  Returns launches (-1: workspace allocation failed).
+bool potrf_dag_usable(const double* B, int64_t ld);
+int potrf_dag(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st);
 // Distributed-Cholesky tile kernels; see sdpc.h.
 int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t ldl, const double* inv, int kb,
                const int32_t* d_err, cudaStream_t st);

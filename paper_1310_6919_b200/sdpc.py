@@ -39,6 +39,9 @@ _SIGS = [
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
     ("sdpc_set_timing", C.c_int, [_P, C.c_int32]),
     ("sdpc_set_truncation", C.c_int, [_P, C.c_int32]),
+    ("sdpc_set_cholesky_schedule", C.c_int, [_P, C.c_int32]),
+    ("sdpc_set_cholesky_trace", C.c_int, [_P, C.c_int64]),
+    ("sdpc_get_cholesky_trace", C.c_int, [_P, _P, C.c_int64, _P]),
     ("sdpc_launch_count", C.c_int64, [_P]),
     ("sdpc_fp64_peak", C.c_int, [C.c_int32, C.c_double, _P, _P]),
     ("sdpc_destroy", C.c_int, [_P]),
@@ -218,6 +221,18 @@ class Handle:
 
     def set_truncation(self, on):
         self._check(lib().sdpc_set_truncation(self.h, int(bool(on))), "sdpc_set_truncation")
+
+    def set_cholesky_schedule(self, task_graph):
+        self._check(lib().sdpc_set_cholesky_schedule(self.h, int(bool(task_graph))), "sdpc_set_cholesky_schedule")
+
+    def set_cholesky_trace(self, cap):
+        self._check(lib().sdpc_set_cholesky_trace(self.h, int(cap)), "sdpc_set_cholesky_trace")
+
+    def get_cholesky_trace(self, cap):
+        out = np.zeros((int(cap), 4), dtype=np.uint64)
+        n = C.c_int64(0)
+        self._check(lib().sdpc_get_cholesky_trace(self.h, _ptr(out), int(cap), C.byref(n)), "sdpc_get_cholesky_trace")
+        return out[: n.value], out.reshape(-1)
 
     def set_timing(self, on):
         self._check(lib().sdpc_set_timing(self.h, int(bool(on))), "sdpc_set_timing")

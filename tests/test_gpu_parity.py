@@ -191,12 +191,14 @@ def test_cholesky_not_pd_reports_leading_minor():
     assert h.scm_cholesky(Bt, 3, raise_not_pd=False) == 3
 
 
-def test_cholesky_not_pd_deep_index():
-    """Failing pivot beyond the first panels (m = 7201): info = 5001."""
+@pytest.mark.parametrize("sched", [1, 0])
+def test_cholesky_not_pd_deep_index(sched):
+    """Failing pivot beyond the first panels (m = 7201): info = 5001 (both schedules)."""
     from instances import gen_config
     from paper_1310_6919_b200 import Handle
     inst = gen_config(2)
     h = Handle.from_instance(inst)
+    h.set_cholesky_schedule(sched)
     m = inst.m
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(3)
@@ -266,13 +268,15 @@ def test_full_config_sampled_columns(cfg):
     assert float(res) < 1e-13
 
 
-@pytest.mark.parametrize("m", [1, 31, 128, 129, 255, 256, 257, 513, 1000, 1311])
-@pytest.mark.parametrize("pad", [0, 1])
-def test_cholesky_random_spd_ragged(m, pad):
-    """(d) alone: random SPD B of sizes around the 128/256 block edges, even and odd ld (the
-    16-byte and 8-byte staging paths); R against LAPACK potrf; strict upper triangle untouched."""
+@pytest.mark.parametrize("m", [1, 31, 128, 129, 255, 256, 257, 383, 513, 1000, 1311, 2100])
+@pytest.mark.parametrize("pad,sched", [(0, 1), (0, 0), (1, 1)])
+def test_cholesky_random_spd_ragged(m, pad, sched):
+    """(d) alone: random SPD B of sizes around the 128/256 block edges; the task-graph kernel (even ld,
+    sched 1), the multi-launch schedule (sched 0) and odd ld (8-byte staging, falls back to the
+    multi-launch schedule); R against LAPACK potrf; strict upper triangle untouched."""
     from tests.helpers import scm_handle
     h = scm_handle(m)
+    h.set_cholesky_schedule(sched)
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(m * 7 + pad)
     G = rng.standard_normal((m, m + 8))
