@@ -46,6 +46,25 @@ def source_hash() -> str:
     return hsh.hexdigest()
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """Experiment helper: build the library with extra -D flags into `out` (not the product library)."""
+    objdir = os.path.join(HERE, "build", "variant")
+    os.makedirs(objdir, exist_ok=True)
+    global FLAGS
+    saved = FLAGS
+    FLAGS = FLAGS + [f"-D{d}" for d in defines]
+    try:
+        with cf.ThreadPoolExecutor(max_workers=min(8, len(sources()))) as ex:
+            objs = list(ex.map(lambda s: _compile(s, objdir, False), sources()))
+    finally:
+        FLAGS = saved
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-ldl", "-lpthread"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return out
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = sources()
     stamp = OUT + ".srchash"

@@ -15,7 +15,7 @@
 // ready), so the scheme is deadlock-free whatever the number of co-resident CTAs.
 //
 // GEMMs: mma.sync m8n8k4 f64 (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind), 8 warps x (32 x 32),
-// operands staged by a 4-stage cp.async.cg pipeline of 16-deep k-chunks.  Data written by other CTAs is
+// operands staged by a double-buffered cp.async.cg pipeline of 32-deep k-chunks.  Data written by other CTAs is
 // read only through L2 (cp.async.cg / ld.global.cg): L1 is not coherent across SMs.  Requires B
 // 16-byte aligned with an even leading dimension (the caller falls back to the multi-launch schedule
 // of k_potrf.cu otherwise).
@@ -35,14 +35,18 @@ namespace dag {
 
 constexpr int NB = 128;          // tile
 constexpr int kThreads = 256;    // 8 warps
-constexpr int kBK = 16;          // k-chunk per pipeline stage
-constexpr int kStages = 4;
+#ifndef SDPC_DAG_BK  // (16-deep x 4 stages measured 2.4% more update time on configs[1])
+#define SDPC_DAG_BK 32
+#define SDPC_DAG_STAGES 2
+#endif
+constexpr int kBK = SDPC_DAG_BK;          // k-chunk per pipeline stage
+constexpr int kStages = SDPC_DAG_STAGES;
 constexpr int kGemmSmem = kStages * kBK * ((NB + 4) + (NB / 2 + 4));  // doubles (both tile shapes)
 // POTRF: the lower 128 x 128 tile as four packed 32-column panels (panel p = rows 32p..127, ld 132 - 32p),
 // the diagonal of L^{-1}, the current 32 x 32 diagonal-block inverse as a full square (later the scratch
 // block of the in-place L^{-1})
 constexpr int kPackN = 32 * (132 + 100 + 68 + 36);
-constexpr int kPotrfSmem = kPackN + NB + 32 * 36;
+constexpr int kPotrfSmem = kPackN + NB + 32 * 36 + 32;
 constexpr int kSmem = kGemmSmem > kPotrfSmem ? kGemmSmem : kPotrfSmem;
 constexpr int kCtl = 32;         // uint32 stride between queue counters (one 128-byte line each)
 constexpr int kQ = 5;            // ready queues
@@ -333,17 +337,19 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
   return __hiloint2double((int)rhi, (int)rlo);
 }
 
-// Warp Cholesky + inverse of the 32 x 32 diagonal block at Ab (ld), lane = row, the row in registers and
-// columns broadcast by shuffles.  Out: strict lower(Ab) <- L; ldiag[a] <- L[a][a]; upper(Ab) incl. the
-// diagonal (row b, column a >= b) <- Linv[a][b]; Dq[a * 33 + b] <- Linv[a][b] (zero above the diagonal).
-// Returns the failing local column or -1 (uniform over the warp).
-__device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double* Dq, int lane) {
+// Warp Cholesky + inverse of the 32 x 32 diagonal block at Ab (ld), lane = row with the row in registers.
+// Per column: the pivot by one shuffle, the scaled column broadcast through shared memory (col, 16-byte
+// aligned, 16-byte loads): no per-element shuffles (SHFL of a double costs ~9 clk of issue, and
+// shuffles make ptxas emit a second, non-converged copy of the code).  Out: strict lower(Ab) <- L;
+// ldiag[a] <- L[a][a]; upper(Ab) incl. the diagonal (row b, column a >= b) <- Linv[a][b];
+// Dq[a * 33 + b] <- Linv[a][b] (zero above the diagonal).  Returns the failing local column or -1.
+__device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double* Dq, double* col, int lane) {
   double row[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * ld] : 0.0;
+  const double2* col2 = reinterpret_cast<const double2*>(col);
   int fail = -1;
   double rinv = 0.0;
-  // branch-free: lanes < j update entries above the diagonal, which are never read
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const double d = shfl_d(row[j], j);
@@ -351,17 +357,28 @@ __device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double
     const double rl = rsqrt_nr(d);
     rinv = lane == j ? rl : rinv;
     row[j] *= rl;
+    if (j < 31) {
+      col[lane] = row[j];
+      __syncwarp();
+      // lanes < k update entries above the diagonal, which are never read
 #pragma unroll
-    for (int k = j + 1; k < 32; ++k) row[k] = fma(-row[j], shfl_d(row[j], k), row[k]);
+      for (int k2 = (j + 1) / 2; k2 < 16; ++k2) {
+        const double2 c = col2[k2];
+        if (2 * k2 > j) row[2 * k2] = fma(-row[j], c.x, row[2 * k2]);
+        row[2 * k2 + 1] = fma(-row[j], c.y, row[2 * k2 + 1]);
+      }
+      __syncwarp();
+    }
   }
   if (fail >= 0) return fail;
-#pragma unroll
-  for (int c = 0; c < 32; ++c)
-    if (c < lane) Ab[lane + c * ld] = row[c];
   double dl = 0.0;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) dl = c == lane ? row[c] : dl;
+  for (int c = 0; c < 32; ++c) {
+    if (c < lane) Ab[lane + c * ld] = row[c];
+    dl = c == lane ? row[c] : dl;
+  }
   ldiag[lane] = dl;
+  col[lane] = rinv;
   __syncwarp();
   // inverse, lane = column c: right-looking forward substitution (x_i final at step i)
   double x[32];
@@ -369,7 +386,7 @@ __device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double
   for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    x[i] *= shfl_d(rinv, i);
+    x[i] *= col[i];
 #pragma unroll
     for (int k = i + 1; k < 32; ++k) x[k] -= Ab[k + i * ld] * x[i];
   }
@@ -418,7 +435,7 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
     const int c0 = 32 * p, ldp = pld(p);
     double* P = S + pofs(p);  // panel p: element (r, c0 + c) at P[(r - c0) + c ldp]
     if (wid == 0) {
-      const int f = wchol32(P, ldp, ldiag + c0, Dq, lane);
+      const int f = wchol32(P, ldp, ldiag + c0, Dq, Dq + 32 * 36, lane);
       if (lane == 0) fail_col = f;
     }
     __syncthreads();
@@ -574,15 +591,18 @@ __global__ void __launch_bounds__(kThreads, 2) chol_dag_kernel(Args a) {
     // role: the first CTAs to arrive elect kChainSms SMs; every CTA on an elected SM serves the chain
     unsigned smid;
     asm("mov.u32 %0, %%smid;" : "=r"(smid));
-    int chain = 0;
-    for (int r = 0; r < kChainSms && !chain; ++r) {
+    // one CTA per elected SM serves the chain; another CTA on an elected SM leaves at once, so the two
+    // halves of a chain TRSM / update never share an SM (-1 = leave, 0 = bulk, 1 = chain)
+    int role = 0;
+    for (int r = 0; r < kChainSms && role == 0; ++r) {
       const unsigned o = atomicCAS(&a.ctl[2 * kQ * kCtl + r], 0u, smid + 1);
-      chain = (o == 0 || o == smid + 1);
+      role = o == 0 ? 1 : (o == smid + 1 ? -1 : 0);
     }
-    s_chain = chain;
+    s_chain = role;
     if (blockIdx.x == 0) push(a, enc(kPotrf, 0, 0, 0, 0));
   }
   __syncthreads();
+  if (s_chain < 0) return;
   const int q0 = s_chain ? 0 : 2, q1 = s_chain ? 2 : kQ;
   if (tid == 32) s_task = pop(a, tk, q0, q1);
   __syncthreads();

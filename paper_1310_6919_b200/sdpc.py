@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdpc.so")
+LIB_PATH = os.environ.get("SDPC_LIB") or os.path.join(_HERE, "libsdpc.so")  # SDPC_LIB: experiments only
 
 SDPC_OK, SDPC_ERR_INVALID_ARG, SDPC_ERR_NOT_PD, SDPC_ERR_OOM, SDPC_ERR_CUDA, SDPC_ERR_NCCL, SDPC_ERR_STATE = range(7)
 
