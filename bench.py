@@ -9,8 +9,11 @@ torus, n = m = 10,000), the configuration the metric is quoted on that fits one 
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
---impl reference times the CPU oracle (oracle/, the only other place bench.py executes it) on a
-bounded sample of the same workload.
+--impl reference times the CPU oracle (oracle/, the only other place bench.py executes it) on the host
+cores: Algorithm 1, the Y factorisation, the SCM columns in a first-come-first-served process pool
+(the paper's Algorithm 2, P:889-914) and LAPACK potrf at the true m.  Configs 0-2 build the full B;
+configs 3-4 fit t_fixed + t_col |cols| on two column samples and extrapolate t_col only.  The same
+measurement is the `cpu_baseline` object of our line.
 """
 from __future__ import annotations
 
@@ -39,11 +42,44 @@ CONFIG_TEXT = {
 FP64_OVER_BF16 = 45.0 / 2250.0
 FALLBACK_BF16 = dict(burst=1590.0, sustained=1400.0)   # B200_PROFILING.md fallback
 FALLBACK_HBM = 6650.0
-# ncu --set full of one gemm_nt_kernel<UpdTri> launch on configs[1] (4290 tiles of 128 x 64, K = 256,
-# 1.80e10 flops): dram__bytes_read.sum + dram__bytes_write.sum = 292.2 MB + 220.2 MB.
-UPD_BYTES_PER_FLOP = (292.243456e6 + 220.247040e6) / (4290 * 128 * 64 * 2 * 256)
-UPD_TRAFFIC_SOURCE = ("profiles/r01/ncu/update_UpdTri_128x64_full.txt: 512.5 MB DRAM read+write for one launch "
-                      "of 1.80e10 flops, scaled by the step's update flops")
+# ncu --set full of one chol_dag_kernel launch on a 10,000^2 SPD matrix (configs[1]'s m): dram__bytes_read.sum +
+# dram__bytes_write.sum per algorithmic flop (m^3/3), scaled to the step's m^3/3 (profiles/r02/ncu/).
+DAG_BYTES_PER_FLOP = (4.226713e9 + 4.040358e9) / (1e4 ** 3 / 3.0)
+DAG_TRAFFIC_SOURCE = ("profiles/r02/ncu/dag_c1_full.txt: 4.23 GB read + 4.04 GB written by one chol_dag_kernel launch "
+                      "at m = 10,000 (3.33e11 flops), scaled by the step's m^3/3")
+
+
+def solve_flops(st, inst, truncated):
+    """Algorithmic flops of the multi-RHS solves (b) for the X-hat and the Y^{-1} factor:
+    per RHS p, forward over the etree reach of p (2 (cc_j + 1) per column j on the path), D scaling (n),
+    backward over all of E (2 nnz(E)) or, with the max-cut truncation, over E[p:, p:].  RHS = the vertices
+    the constraints touch (elimination ids).  Computed on the host from the structure."""
+    import numpy as np
+    n = int(st["n"])
+    colptr = np.asarray(st["colptr"], dtype=np.int64)
+    parent = np.asarray(st["parent"], dtype=np.int64)
+    perm = np.asarray(st["perm"], dtype=np.int64)
+    iperm = np.empty(n, dtype=np.int64)
+    iperm[perm] = np.arange(n)
+    w = np.diff(colptr).astype(np.float64)                   # cc_j + 1
+    rows = np.concatenate([inst.a_row[inst.a_ptr[1]:], inst.a_col[inst.a_ptr[1]:]])
+    rhs = np.zeros(n, dtype=bool)
+    rhs[iperm[np.unique(rows)]] = True
+    # reach(p) = etree path p -> root; count of RHS below each node = RHS in its subtree (children < parent)
+    cnt = rhs.astype(np.float64)
+    for j in range(n):
+        if parent[j] >= 0:
+            cnt[parent[j]] += cnt[j]
+    fwd = 2.0 * float(np.sum(cnt * w))
+    nnz = float(colptr[-1])
+    nr = float(rhs.sum())
+    if truncated:
+        # sum over RHS p of nnz(E[p:, p:]) = sum_j (number of RHS p <= j) (cc_j + 1)
+        bwd = 2.0 * float(np.sum(np.cumsum(rhs) * w))
+    else:
+        bwd = 2.0 * nnz * nr
+    per_factor = fwd + bwd + n * nr
+    return per_factor, per_factor
 
 
 def peaks():
@@ -151,7 +187,7 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     l0 = h.launch_count()
-    times, phases = [], []
+    times, phases, ktimes = [], [], []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -163,6 +199,7 @@ def run_ours(args, rank, world, local_rank):
             ev1.synchronize()
             times.append(ev0.elapsed_time(ev1))
             phases.append(h.phase_times())
+            ktimes.append(h.kernel_times())
     torch.cuda.synchronize()
     launches = h.launch_count() - l0
     ms = statistics.mean(times)
@@ -203,6 +240,7 @@ def run_ours(args, rank, world, local_rank):
         return None
     pk = peaks()
     ph = [statistics.mean(p[i] for p in phases) for i in range(8)]
+    kt = [statistics.mean(p[i] for p in ktimes) for i in range(8)]
     upd_ms, n_upd, upd_flops = ph[5], ph[6], ph[7]
     fp64_derived = pk["bf16_sus"] * FP64_OVER_BF16
     achieved = upd_flops / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else None
@@ -211,10 +249,32 @@ def run_ours(args, rank, world, local_rank):
         dmma, dfma = fp64_peak(local_rank, 1500.0)
     # roof = the larger of the derived FP64 figure and the DMMA throughput measured on this GPU
     fp64_peak_tf = max(fp64_derived, dmma or 0.0)
-    peak_src = (f"measured DMMA microbenchmark on this GPU ({dmma:.1f} TF/s; > derived {fp64_derived:.1f} = "
-                f"{pk['src']} bf16 sustained {pk['bf16_sus']} x nominal FP64/BF16 45/2250)"
+    peak_src = (f"builder-measured DMMA microbenchmark on this GPU ({dmma:.1f} TF/s, sdpc_fp64_peak; MEASURED_PEAKS "
+                f"has no FP64 figure; > derived {fp64_derived:.1f} = {pk['src']} bf16 sustained {pk['bf16_sus']} x "
+                f"nominal FP64/BF16 45/2250)"
                 if dmma and dmma > fp64_derived else
                 f"{pk['src']} bf16 sustained {pk['bf16_sus']} x FP64/BF16 nominal 45/2250")
+    # per-phase roofline fractions (SURVEY §8(d) algorithmic work; kernel windows from CUDA events)
+    trunc = inst.kind == "maxcut"
+    fx, fy = solve_flops(st, inst, trunc)
+    bbytes = 8.0 * entries(m)
+    phase_roof = {
+        "b_solve_x": {"flops": fx, "ms": kt[0], "tflops": fx / (kt[0] * 1e-3) / 1e12 if kt[0] > 0 else None},
+        "b_solve_y": {"flops": fy, "ms": kt[1], "tflops": fy / (kt[1] * 1e-3) / 1e12 if kt[1] > 0 else None},
+        "c_accumulate": {"bytes": bbytes, "ms": kt[2], "gbs": bbytes / (kt[2] * 1e-3) / 1e9 if kt[2] > 0 else None},
+        "d_cholesky": {"flops": m ** 3 / 3.0, "ms": kt[3],
+                       "tflops": m ** 3 / 3.0 / (kt[3] * 1e-3) / 1e12 if kt[3] > 0 else None},
+        "note": ("(b): SURVEY 8(d) flops per RHS (etree-reach forward + backward over nnz(E[p:,p:]) when "
+                 "max-cut truncation is on, + D scaling) over the solved RHS, per launch window (the X-hat "
+                 "window overlaps (a2)); FP64 roof = the line's peak.  (c): B lower triangle written once "
+                 "(8 m(m+1)/2 bytes) over the accumulate kernel; HBM roof = MEASURED_PEAKS hbm_gbs.  (d): m^3/3 "
+                 "over the Cholesky kernel."),
+    }
+    for key in ("b_solve_x", "b_solve_y", "d_cholesky"):
+        v = phase_roof[key]["tflops"]
+        phase_roof[key]["frac_fp64"] = v / fp64_peak_tf if v else None
+    gbs = phase_roof["c_accumulate"]["gbs"]
+    phase_roof["c_accumulate"]["frac_hbm"] = gbs / pk["hbm"] if gbs else None
     value = world * entries(m) / (ms * 1e-3)
     line = {
         "metric": METRIC,
@@ -241,22 +301,23 @@ def run_ours(args, rank, world, local_rank):
                       "note": "sdpc_scm_solve (R R^T) dz = g, one RHS, with the factor of the step (not in the metric)"},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / args.steps,
-        "roofline": {"kernel": "gemm_nt_kernel<kModeUpdTri> (SCM Cholesky trailing update, K = 256, DMMA)",
+        "roofline": {"kernel": "chol_dag_kernel (SCM Cholesky (d): one persistent launch over the 128-tile task "
+                               "graph, DMMA trailing updates)",
                      "bound": "tensor", "achieved": achieved, "peak": fp64_peak_tf, "unit": "TFLOP/s",
                      "frac": (achieved / fp64_peak_tf) if achieved else None,
-                     # DRAM bytes of the step's update launches, from the measured bytes/flop of one
-                     # profiled launch (ncu --set full; C read once + written once per tile, panel in L2)
-                     "traffic": UPD_BYTES_PER_FLOP * upd_flops,
-                     "traffic_source": UPD_TRAFFIC_SOURCE,
+                     "traffic": (DAG_BYTES_PER_FLOP * upd_flops) if DAG_BYTES_PER_FLOP else None,
+                     "traffic_source": DAG_TRAFFIC_SOURCE,
                      "peak_source": peak_src,
                      "launches_per_step": n_upd, "flops_per_step": upd_flops,
                      "fp64_microbench_tflops": {"dmma": dmma, "dfma": dfma}},
+        "phase_roofline": phase_roof,
         "e2e": {"value": world * entries(m) / (e2e_ms * 1e-3), "unit": "B-entries/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(2 * 8 * inst.nnzE),
                 "d2h_bytes_per_step": int(8 * m + 4),
                 "api": "sdpc_iteration_host (host xbar_E, y_E in; diag(R), info out)"},
     }
     if not args.no_cpu_baseline:
+        cpu_baseline(inst, args)                 # warm-up (page cache, forked pool, BLAS init): not reported
         line["cpu_baseline"] = cpu_baseline(inst, args)
     return line
 
@@ -372,8 +433,49 @@ def run_ours_dist(args, rank, world, local_rank):
 
 # ----------------------------------------------------------------------------- oracle (reference arm)
 
-def cpu_baseline(inst, args, budget_cols=None):
-    """Time the oracle as it stands on a bounded sample; extrapolate to one full iteration."""
+_POOL_STATE = {}
+
+
+def _pool_init():
+    """Single-threaded workers: BLAS threads inside a worker would oversubscribe the cores."""
+    try:
+        from threadpoolctl import threadpool_limits
+        _POOL_STATE["limits"] = threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _pool_columns(cols):
+    """Worker of the FCFS column pool: full SCM columns for a block of constraint indices."""
+    from oracle import scm as SCM
+    st = _POOL_STATE
+    return cols, SCM.scm_columns(st["inst"], cols, st["solver"], prep=st["prep"])
+
+
+def _fcfs_columns(inst, solver, prep, cols, procs, block=32):
+    """Algorithm 2: the SCM columns in a first-come-first-served queue over `procs` worker
+    processes (forked: the oracle's factors are shared copy-on-write), single-threaded solves inside a
+    worker.  Returns B[:, cols] (m x len(cols)) and the wall time."""
+    import multiprocessing as mp
+
+    import numpy as np
+    _POOL_STATE.update(inst=inst, solver=solver, prep=prep)
+    blocks = [cols[a:a + block] for a in range(0, len(cols), block)]
+    pos = {l: a for a, l in enumerate(cols)}
+    out = np.zeros((inst.m, len(cols)))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs, initializer=_pool_init) as pool:
+        for bc, val in pool.imap_unordered(_pool_columns, blocks):
+            out[:, [pos[l] for l in bc]] = val
+    return out, time.perf_counter() - t0
+
+
+def cpu_baseline(inst, args, full=None):
+    """The CPU oracle (oracle/, as it stands) timed for one iteration on this host's cores:
+    Algorithm 1 (oracle), the Y factorisation, the SCM columns by sparse solves in an FCFS process pool
+    (Algorithm 2), and LAPACK potrf at the true m.  Configs 0-2 build the full B (no extrapolation);
+    larger configs time two column samples (1x and 3x) and fit t = t_fixed + t_col |cols|, scaling only
+    t_col to m columns (labelled extrapolated)."""
     import numpy as np
 
     from oracle import algorithm1 as A1, cholesky as CH, scm as SCM, symbolic as SYM
@@ -387,26 +489,52 @@ def cpu_baseline(inst, args, budget_cols=None):
     t0 = time.perf_counter()
     solver = SCM.ColumnSolver(S, L, D, inst.y, inst.perm)
     t_fac = time.perf_counter() - t0
-    ncols = budget_cols or min(inst.m, 64)
-    cols = list(range(0, inst.m, max(1, inst.m // ncols)))[:ncols]
     t0 = time.perf_counter()
-    SCM.scm_columns(inst, cols, solver)
-    t_cols = time.perf_counter() - t0
-    msub = min(inst.m, 4000)
-    rng = np.random.default_rng(0)
-    G = rng.standard_normal((msub, msub))
-    Bs = G @ G.T + msub * np.eye(msub)
-    t0 = time.perf_counter()
-    CH.potrf_lower(Bs)
-    t_chol = time.perf_counter() - t0
+    prep = SCM.column_prep(inst)
+    t_prep = time.perf_counter() - t0
     m = inst.m
-    t_iter = t_a1 + t_fac + t_cols * (m / len(cols)) + t_chol * (m / msub) ** 3
+    if full is None:
+        full = args.config in (0, 1, 2)
+    if full:
+        B, t_cols = _fcfs_columns(inst, solver, prep, list(range(m)), cores)
+        t0 = time.perf_counter()
+        CH.potrf_lower(B)
+        t_chol = time.perf_counter() - t0
+        t_build = t_prep + t_cols
+        how = (f"full B ({m} columns) by the FCFS pool ({t_cols:.2f} s) + LAPACK potrf of that B, m = {m} "
+               f"({t_chol:.2f} s)")
+    else:
+        rng = np.random.default_rng(1)
+        n1 = max(2 * cores, 64)
+        c1 = sorted(rng.choice(m, size=min(n1, m), replace=False).tolist())
+        c3 = sorted(rng.choice(m, size=min(3 * n1, m), replace=False).tolist())
+        _, ta = _fcfs_columns(inst, solver, prep, c1, cores)
+        _, tb = _fcfs_columns(inst, solver, prep, c3, cores)
+        t_col = max(tb - ta, 1e-9) / max(len(c3) - len(c1), 1)
+        t_fixed = max(ta - t_col * len(c1), 0.0)
+        t_build = t_prep + t_fixed + t_col * m
+        # potrf at the true m if host memory allows (2 copies of m^2 doubles), else m^3-scaled from m/2
+        try:
+            avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        except (ValueError, OSError):
+            avail = 0
+        msub = m if 3 * 8 * m * m < avail else m // 2
+        G = rng.standard_normal((msub, 64))
+        Bs = G @ G.T / 64 + np.eye(msub)
+        del G
+        t0 = time.perf_counter()
+        CH.potrf_lower(Bs)
+        t_chol = (time.perf_counter() - t0) * (m / msub) ** 3
+        del Bs
+        how = (f"columns: two FCFS-pool samples ({len(c1)} cols {ta:.2f} s, {len(c3)} cols {tb:.2f} s) fitted "
+               f"t = {t_fixed:.2f} s + {t_col * 1e3:.3f} ms x cols, EXTRAPOLATED to {m} columns; LAPACK potrf of "
+               f"an SPD {msub}x{msub} ({'true m' if msub == m else 'm/2, x8: extrapolated'}, {t_chol:.2f} s)")
+    t_iter = t_a1 + t_fac + t_build + t_chol
     return {"value": entries(m) / t_iter, "unit": "B-entries/s", "s_per_iter": t_iter, "cores": cores,
             "kind": "oracle",
-            "sample": (f"oracle Algorithm 1 on all cliques ({t_a1:.2f} s) + Y factorization ({t_fac:.2f} s) + "
-                       f"{len(cols)} of {m} SCM columns by sparse solves ({t_cols:.2f} s, x{m / len(cols):.0f}) + "
-                       f"LAPACK potrf of a {msub}x{msub} SPD matrix ({t_chol:.2f} s, x(m/{msub})^3); "
-                       f"extrapolated to one iteration; symbolic setup {t_sym:.2f} s excluded")}
+            "phases_s": {"a1_algorithm1": t_a1, "y_factor": t_fac, "scm_columns": t_build, "potrf": t_chol},
+            "sample": (f"oracle on {cores} host cores: Algorithm 1 on all cliques ({t_a1:.2f} s), Y factor ({t_fac:.2f} s), "
+                       f"{how}; one-time symbolic setup {t_sym:.2f} s excluded")}
 
 
 def run_reference(args, rank, world):
@@ -415,17 +543,20 @@ def run_reference(args, rank, world):
     from instances import gen_config
     inst = gen_config(args.config, seed=args.seed)
     vals = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(inst, args, budget_cols=16)
-        if i >= args.warmup:
+    # CPU steps have no caches to warm beyond the first: at most one warm-up step
+    warm = min(args.warmup, 1)
+    for i in range(warm + args.steps):
+        cb = cpu_baseline(inst, args)
+        if i >= warm:
             vals.append(cb)
     ms = statistics.mean(v["s_per_iter"] for v in vals) * 1e3
     value = entries(inst.m) / (ms * 1e-3)
     last = vals[-1]
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "B-entries/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "steps": args.steps, "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "n": inst.n, "m": inst.m, "seed": args.seed},
+            "steps_s": [v["s_per_iter"] for v in vals],
             "cpu_baseline": {"value": value, "unit": "B-entries/s", "cores": last["cores"], "kind": "oracle",
                              "sample": last["sample"]},
             "e2e": {"value": value, "unit": "B-entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

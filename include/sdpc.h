@@ -252,6 +252,12 @@ sdpc_status sdpc_iteration_host(sdpc_handle h, const double* xbar_E, const doubl
  * start of the iteration to the end of (a1), (a2) and (b) respectively. */
 sdpc_status sdpc_get_phase_times(sdpc_handle h, double* t /* [8] */);
 
+/* Kernel windows (ms) of the last sdpc_iteration, CUDA events on the launching streams: t[0] = the X-hat
+ * solve launch ((b), factor 1), t[1] = the Y^{-1} solve launch ((b), factor 2; runs concurrently with
+ * t[0]'s tail), t[2] = the accumulate (c), t[3] = the SCM Cholesky kernel(s) (d), t[4] = start -> (a1)
+ * done, t[5] = start -> (a2) done, t[6], t[7] reserved (0).  Used for the per-phase roofline fractions. */
+sdpc_status sdpc_get_kernel_times(sdpc_handle h, double* t /* [8] */);
+
 /* Enable (1) / disable (0) per-phase event timing (default on; costs a few events per call). */
 sdpc_status sdpc_set_timing(sdpc_handle h, int32_t on);
 

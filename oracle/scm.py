@@ -170,18 +170,25 @@ class ColumnSolver:
         return ynew[self.iperm, :]
 
 
-def scm_columns(inst, cols, solver: ColumnSolver, chunk=128):
-    """Full columns B[:, l] (all k) for the constraint indices l in `cols` (0-based).
-
-    The solves x_p, y_q for all nonzero columns of the sampled A_l are done first, in
-    multi-RHS chunks (same arithmetic as one solve per RHS, Algorithm 2 Step 3-3).
-    """
-    m = inst.m
+def column_prep(inst):
+    """Per-instance tables of scm_columns (constraint entries, small/large split), computed once."""
     ents = sym_entries(inst)
     sizes = np.array([e[0].size for e in ents])
     small = np.flatnonzero(sizes <= LARGE)
     large = np.flatnonzero(sizes > LARGE)
     I, J, V = _padded(ents, small)
+    return ents, small, large, I, J, V
+
+
+def scm_columns(inst, cols, solver: ColumnSolver, chunk=128, prep=None):
+    """Full columns B[:, l] (all k) for the constraint indices l in `cols` (0-based).
+
+    The solves x_p, y_q for all nonzero columns of the sampled A_l are done first, in
+    multi-RHS chunks (same arithmetic as one solve per RHS, Algorithm 2 Step 3-3).
+    `prep` = column_prep(inst) (recomputed when omitted).
+    """
+    m = inst.m
+    ents, small, large, I, J, V = prep if prep is not None else column_prep(inst)
     ps = np.unique(np.concatenate([ents[l][0] for l in cols]))
     qs = np.unique(np.concatenate([ents[l][1] for l in cols]))
     X = np.concatenate([solver.x(ps[a:a + chunk]) for a in range(0, ps.size, chunk)], axis=1)

@@ -558,6 +558,12 @@ sdpc_status sdpc_get_phase_times(sdpc_handle h, double* t) {
   return SDPC_OK;
 }
 
+sdpc_status sdpc_get_kernel_times(sdpc_handle h, double* t) {
+  if (!h || !t) return SDPC_ERR_INVALID_ARG;
+  for (int i = 0; i < 8; ++i) t[i] = h->ktimes[i];
+  return SDPC_OK;
+}
+
 sdpc_status sdpc_factor_xinv(sdpc_handle h, const double* xbar_E, void* stream) {
   if (!h || !xbar_E) return SDPC_ERR_INVALID_ARG;
   CK(cudaSetDevice(h->device));
@@ -759,10 +765,13 @@ sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_
   // (each CTA walks several panels) so that about a third of the SMs stay free for the (a2) levels
   // on the high-priority stream; shallow trees (block-arrow: 2 levels) keep the whole GPU
   const bool deep = h->a2lev.size() >= 8;
+  if (h->timing) CK(cudaEventRecord(h->ev[8], st));
   h->launches += launch_inverse_panels(h, st, 0, 1, deep ? kSolveCtasDuringA2 : 0);
+  if (h->timing) CK(cudaEventRecord(h->ev[9], st));
   h->launches += launch_ldl_y(h, y_E, h->st3, h->d_err + 1, 1);
   if (h->timing) CK(cudaEventRecord(h->ev[2], h->st3));
   h->launches += launch_inverse_panels(h, h->st3, 1, 1);
+  if (h->timing) CK(cudaEventRecord(h->ev[10], h->st3));
   CK(cudaEventRecord(h->it_join, h->st3));
   CK(cudaStreamWaitEvent(st, h->it_join, 0));
   if (h->timing) CK(cudaEventRecord(h->ev[4], st));
@@ -789,6 +798,13 @@ sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_
     h->times[5] = tu;
     h->times[6] = nu;
     h->times[7] = fl;
+    // kernel windows: X-hat solve launch(es), Y^{-1} solve launch(es), accumulate, Cholesky kernel
+    h->ktimes[0] = elapsed(h->ev[8], h->ev[9]);
+    h->ktimes[1] = elapsed(h->ev[2], h->ev[10]);
+    h->ktimes[2] = h->times[3];
+    h->ktimes[3] = tu;
+    h->ktimes[4] = h->times[0];
+    h->ktimes[5] = h->times[1];
   }
   *info = 0;
   if (fl3[0] != kNoError) {

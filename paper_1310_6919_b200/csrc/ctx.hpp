@@ -149,6 +149,7 @@ struct sdpc_ctx {
   int64_t last_info = 0;
   bool timing = true;
   double times[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double ktimes[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // sdpc_get_kernel_times
   int64_t launches = 0;
   cudaEvent_t ev[16];
   std::vector<cudaEvent_t> upd_ev;  // per trailing-update launch (pairs)

@@ -37,6 +37,7 @@ _SIGS = [
     ("sdpc_iteration", C.c_int, [_P, _P, _P, _P, C.c_int64, _P, _P]),
     ("sdpc_iteration_host", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
+    ("sdpc_get_kernel_times", C.c_int, [_P, _P]),
     ("sdpc_set_timing", C.c_int, [_P, C.c_int32]),
     ("sdpc_set_truncation", C.c_int, [_P, C.c_int32]),
     ("sdpc_set_cholesky_schedule", C.c_int, [_P, C.c_int32]),
@@ -217,6 +218,11 @@ class Handle:
     def phase_times(self):
         t = (C.c_double * 8)()
         self._check(lib().sdpc_get_phase_times(self.h, t), "sdpc_get_phase_times")
+        return list(t)
+
+    def kernel_times(self):
+        t = (C.c_double * 8)()
+        self._check(lib().sdpc_get_kernel_times(self.h, t), "sdpc_get_kernel_times")
         return list(t)
 
     def set_truncation(self, on):
