@@ -352,3 +352,11 @@ def gen_config(i: int, seed: int = 0, cache: bool = True) -> Instance:
         except OSError:
             pass
     return inst
+
+
+def direction_G(inst: Instance, seed: int = 0, scale: float = 0.1) -> np.ndarray:
+    """Synthetic input G of the search direction (PAPER.md P:375-385: the matrix G in g_k and dY;
+    DESIGN.md reading: a residual matrix supplied by the caller) as lower values on E (E's CSC order):
+    N(0, scale^2) entries, seeded (SeedSequence([seed, 7])).  No method arithmetic."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 7]))
+    return scale * rng.standard_normal(int(inst.colptr[-1]))

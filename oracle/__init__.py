@@ -18,9 +18,12 @@ slow and fp64, each function citing the PAPER.md passage it follows:
 * scm.py       - B_kl = trace(A_k X-hat A_l Y^{-1}) (P:380 Eq. SCM), dense
                  mode and sampled-column mode via per-RHS solves (P:686-688 Eq. newSCM2).
 * cholesky.py  - LAPACK potrf of B (type (i)).
+* direction.py - the HKM search direction as printed: g, dz (Eq. SCE), dY, dX-hat and dX on
+                 E (P-MATRIX, Eq. newdX/newdX2), mu, step lengths
+                 alpha_p per clique (Eq. primal_length2) and alpha_d.
 
 Parity status of every function is listed in DESIGN.md §Oracle pins; every
 function here is pinned by a `-m "not gpu"` test against values the paper or
 mathematics fixes (tests/test_oracle_*.py).  None is "parity unpinned".
 """
-from . import symbolic, algorithm1, ldl, scm, cholesky  # noqa: F401
+from . import symbolic, algorithm1, ldl, scm, cholesky, direction  # noqa: F401
