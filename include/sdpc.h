@@ -265,6 +265,40 @@ sdpc_status sdpc_set_timing(sdpc_handle h, int32_t on);
 int64_t sdpc_launch_count(sdpc_handle h);
 
 /*
+ * sdpc_search_direction - the HKM search direction of the iteration,
+ * after sdpc_scm_build (or sdpc_iteration) and sdpc_scm_cholesky on the same handle, as printed in
+ * PAPER.md §2.2:
+ *   g_k  = A_k . (beta_mu Y^{-1} - X-hat - X-hat G Y^{-1})   (k = 1..m; A_k . X-hat = A_k . X-bar on E)
+ *   B dz = g            (forward / backward substitution with R, the factor left in B by the Cholesky)
+ *   dY   = G - sum_k A_k dz_k                                on E
+ *   dX   = (dX-hat + dX-hat^T) / 2 on E, column k of dX-hat = beta_mu Y^{-1} e_k - X-hat e_k
+ *          - X-hat dY Y^{-1} e_k   (P-MATRIX, Eq. newdX2; only entries on E are kept)
+ *   xbar_E, G_E : DEVICE [nnzE] X-bar and the residual matrix G on E (E's CSC order).  G is taken as
+ *                 given (the paper prints G = A_0 - sum A_k z_k).
+ *   beta_mu     : beta * mu, mu = X . Y / n.
+ *   R, ldr      : DEVICE, the SCM factor (lower triangle of the B passed to sdpc_scm_cholesky).
+ *   g, dz       : DEVICE [m] out;  dY_E, dX_E : DEVICE [nnzE] out.
+ * Uses the handle's X-hat / Y^{-1} columns (re-solved in full when the build used the truncated max-cut
+ * sweep) and an extra dense panel buffer (the size of one of them).  Synchronous.  Errors: STATE
+ * (nranks > 1, no build, or some vertex in no constraint: every vertex must be a solve RHS), OOM.
+ */
+sdpc_status sdpc_search_direction(sdpc_handle h, const double* xbar_E, const double* G_E, double beta_mu,
+                                  const double* R, int64_t ldr, double* g, double* dz, double* dY_E,
+                                  double* dX_E, void* stream);
+
+/*
+ * sdpc_step_lengths - Step 3 of the PDIPM with the completion (Eq. primal_length2):
+ *   alpha_p = min_r max{alpha in (0,1] : X-bar_{C_rC_r} + alpha dX_{C_rC_r} >= 0}  (cliques = supernodes)
+ *   alpha_d = max{alpha in (0,1] : Y + alpha dY >= 0}
+ * by bisection with attempted Cholesky factorisations: per clique block for alpha_p (one CTA per clique,
+ * 40 steps, the returned value is feasible and within 2^-40 of the boundary), the sparse LDL^T of
+ * Y + alpha dY on E for alpha_d (30 steps, within 2^-30).  All inputs DEVICE [nnzE] on E; alpha_p and
+ * alpha_d HOST out.  The handle's Y factor is overwritten (a later sdpc_scm_build refactors Y).
+ */
+sdpc_status sdpc_step_lengths(sdpc_handle h, const double* xbar_E, const double* dX_E, const double* y_E,
+                              const double* dY_E, double* alpha_p, double* alpha_d, void* stream);
+
+/*
  * FP64 roof microbenchmarks (N10): sustained DMMA (mma.sync m8n8k4 f64 -> DMMA.8x8x4) and
  * DFMA throughput over all SMs for about `ms` milliseconds each.  Outputs TFLOP/s.
  */

@@ -227,6 +227,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   std::vector<int64_t> cptr(m + 1, 0);
   std::vector<int32_t> ci, cj;
   std::vector<double> cv;
+  std::vector<uint8_t> cmirror;  // 1 for the mirrored copy of an off-diagonal entry
   bool maxcut = true;
   std::vector<int32_t> vrow(m), col_cons(n, -1);
   std::vector<double> aval(m);
@@ -247,10 +248,12 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
       ci.push_back(r);
       cj.push_back(c);
       cv.push_back(x.second);
+      cmirror.push_back(0);
       if (r != c) {
         ci.push_back(c);
         cj.push_back(r);
         cv.push_back(x.second);
+        cmirror.push_back(1);
       }
     }
     cptr[k + 1] = (int64_t)ci.size();
@@ -306,6 +309,61 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     std::sort(tmp.begin(), tmp.end());
     reach_sn.insert(reach_sn.end(), tmp.begin(), tmp.end());
     reach_ptr[P + 1] = (int32_t)reach_sn.size();
+  }
+
+  // ---- search direction tables (k_direction.cu): all supernodes; symmetric CSR of E with the E offset
+  // of each entry; per E entry the constraint entries on it (dY = G - sum_k A_k dz_k); per
+  // expanded constraint entry its E offset (X-bar values in g_k)
+  auto epos = [&](int32_t a, int32_t b) -> int32_t {  // offset of (max, min) in E's CSC, -1 if absent
+    const int32_t hi = std::max(a, b), lo = std::min(a, b);
+    const int32_t* beg = S.rowind.data() + S.colptr[lo];
+    const int32_t* end = S.rowind.data() + S.colptr[lo + 1];
+    const int32_t* it = std::lower_bound(beg, end, hi);
+    return (it != end && *it == hi) ? (int32_t)(it - S.rowind.data()) : -1;
+  };
+  std::vector<int32_t> all_sn(ns);
+  for (int32_t r = 0; r < ns; ++r) all_sn[r] = r;
+  std::vector<int32_t> sym_ptr(n + 1, 0), sym_col, sym_pos;
+  {
+    const int64_t nnzE = S.nnzE();
+    for (int32_t j = 0; j < n; ++j)
+      for (int64_t q = S.colptr[j]; q < S.colptr[j + 1]; ++q) {
+        ++sym_ptr[S.rowind[q] + 1];
+        if (S.rowind[q] != j) ++sym_ptr[j + 1];
+      }
+    for (int32_t i = 0; i < n; ++i) sym_ptr[i + 1] += sym_ptr[i];
+    sym_col.resize(sym_ptr[n]);
+    sym_pos.resize(sym_ptr[n]);
+    std::vector<int32_t> fill(sym_ptr.begin(), sym_ptr.end() - 1);
+    for (int32_t j = 0; j < n; ++j)
+      for (int64_t q = S.colptr[j]; q < S.colptr[j + 1]; ++q) {
+        const int32_t i = S.rowind[q];
+        sym_col[fill[i]] = j;
+        sym_pos[fill[i]++] = (int32_t)q;
+        if (i != j) {
+          sym_col[fill[j]] = i;
+          sym_pos[fill[j]++] = (int32_t)q;
+        }
+      }
+    (void)nnzE;
+  }
+  std::vector<int32_t> ecs_ptr(S.nnzE() + 1, 0), ecs_k, cons_epos(ci.size(), -1);
+  std::vector<double> ecs_val;
+  {
+    std::vector<std::pair<int32_t, std::pair<int32_t, double>>> lst;  // (E offset, (k, value))
+    for (int32_t k = 0; k < m; ++k)
+      for (int64_t e2 = cptr[k]; e2 < cptr[k + 1]; ++e2) {
+        const int32_t q = epos(ci[e2], cj[e2]);
+        cons_epos[e2] = q;
+        if (q >= 0 && !cmirror[e2]) lst.push_back({q, {k, cv[e2]}});
+      }
+    std::stable_sort(lst.begin(), lst.end(), [](auto& x, auto& y) { return x.first < y.first; });
+    for (auto& x : lst) {
+      ++ecs_ptr[x.first + 1];
+      ecs_k.push_back(x.second.first);
+      ecs_val.push_back(x.second.second);
+    }
+    for (int64_t q = 0; q < S.nnzE(); ++q) ecs_ptr[q + 1] += ecs_ptr[q];
   }
 
   // ---- staged-rows accumulation (one rank, every vertex a RHS slot in order): per small constraint
@@ -388,6 +446,14 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(d.reach_sn, reach_sn);
   UP(d.rhs, rhs);
   UP(d.slot_of, slot_of);
+  UP(d.all_sn, all_sn);
+  UP(d.sym_ptr, sym_ptr);
+  UP(d.sym_col, sym_col);
+  UP(d.sym_pos, sym_pos);
+  UP(d.ecs_ptr, ecs_ptr);
+  UP(d.ecs_k, ecs_k);
+  UP(d.ecs_val, ecs_val);
+  UP(d.cons_epos, cons_epos);
   h->slot_of_host = slot_of;
   UP(h->d_ws_off, ws_off);
   UP(h->d_pre, pre);
@@ -449,7 +515,8 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
   DevSym& d = h->d;
   void* ptrs[] = {d.colptr, d.rowind, d.super_ptr, d.snc, d.sns, d.sparent, d.panel_off, d.e2p, d.umap_off,
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
-                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, h->d_ws_off, h->d_pre, h->d_pre_child,
+                  d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, d.all_sn, d.sym_ptr, d.sym_col, d.sym_pos, d.ecs_ptr, d.ecs_k,
+                  d.ecs_val, d.cons_epos, h->Uh, h->dir_ws, h->d_step_off, h->step_ws, h->d_amin, h->ytmp, h->d_ws_off, h->d_pre, h->d_pre_child,
                   h->d_pre_parent, h->d_zero_list,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
@@ -905,6 +972,60 @@ sdpc_status sdpc_scm_solve(sdpc_handle h, const double* R, int64_t ldr, double* 
   }
   h->launches += scm_solve(R, ldr, h->S.m, G, ldg, nrhs, h->sce_ws, st);
   CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_search_direction(sdpc_handle h, const double* xbar_E, const double* G_E, double beta_mu,
+                                  const double* R, int64_t ldr, double* g, double* dz, double* dY_E, double* dX_E,
+                                  void* stream) {
+  if (!h || !xbar_E || !G_E || !R || !g || !dz || !dY_E || !dX_E || ldr < h->S.m) return SDPC_ERR_INVALID_ARG;
+  if (h->nranks != 1) return SDPC_ERR_STATE;
+  if (!h->have_x || !h->have_y || !h->Xh) return SDPC_ERR_STATE;
+  if (h->d.nrhs != h->S.n) {
+    h->err = "search direction needs every vertex as a solve RHS (some vertex is in no constraint)";
+    return SDPC_ERR_STATE;
+  }
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->timing) CK(cudaEventRecord(h->ev[12], st));
+  int l = direction_g(h, xbar_E, G_E, beta_mu, g, st);
+  if (l < 0) return SDPC_ERR_OOM;
+  h->launches += l;
+  const int m = h->S.m;
+  if (h->sce_cap < 1) {
+    if (h->sce_ws) cudaFree(h->sce_ws);
+    h->sce_ws = nullptr;
+    CK(dalloc(&h->sce_ws, (size_t)128));
+    h->sce_cap = 1;
+  }
+  CK(cudaMemcpyAsync(dz, g, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+  h->launches += scm_solve(R, ldr, m, dz, m, 1, h->sce_ws, st);  // B dz = g (Eq. SCE)
+  if (h->timing) CK(cudaEventRecord(h->ev[13], st));
+  l = direction_dY_dX(h, xbar_E, G_E, beta_mu, dz, dY_E, dX_E, st);
+  if (l < 0) return SDPC_ERR_OOM;
+  h->launches += l;
+  if (h->timing) CK(cudaEventRecord(h->ev[14], st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (h->timing) {
+    h->ktimes[6] = elapsed(h->ev[12], h->ev[13]);  // g + SCE solve
+    h->ktimes[7] = elapsed(h->ev[13], h->ev[14]);  // dY + P-MATRIX
+  }
+  return SDPC_OK;
+}
+
+sdpc_status sdpc_step_lengths(sdpc_handle h, const double* xbar_E, const double* dX_E, const double* y_E,
+                              const double* dY_E, double* alpha_p, double* alpha_d, void* stream) {
+  if (!h || !xbar_E || !dX_E || !y_E || !dY_E || !alpha_p || !alpha_d) return SDPC_ERR_INVALID_ARG;
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int l = primal_step(h, xbar_E, dX_E, alpha_p, st);
+  if (l < 0) return SDPC_ERR_CUDA;
+  h->launches += l;
+  l = dual_step(h, y_E, dY_E, alpha_d, 30, st);
+  if (l < 0) return SDPC_ERR_CUDA;
+  h->launches += l;
   CK(cudaGetLastError());
   return SDPC_OK;
 }

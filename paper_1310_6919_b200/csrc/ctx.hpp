@@ -47,6 +47,16 @@ struct DevSym {
   int32_t* rhs = nullptr;
   int32_t* slot_of = nullptr;
   int32_t nrhs = 0;
+  int32_t* all_sn = nullptr;     // 0 .. nsuper-1 (full forward sweep of a dense RHS panel)
+  // search direction (k_direction.cu): symmetric CSR of E (row i: columns j with (i, j) or (j, i) in E,
+  // sym_pos = offset of that entry in E's CSC value order); per E entry the constraint entries on it
+  int32_t* sym_ptr = nullptr;
+  int32_t* sym_col = nullptr;
+  int32_t* sym_pos = nullptr;
+  int32_t* ecs_ptr = nullptr;    // [nnzE + 1]
+  int32_t* ecs_k = nullptr;      // constraint (0-based)
+  double* ecs_val = nullptr;     // value of its entry (lower triplet, duplicates listed separately)
+  int32_t* cons_epos = nullptr;  // per symmetric-expanded constraint entry (DevCons order): E offset
 };
 
 // Size classes of the batched per-clique kernels ((a1) and (a2)).
@@ -117,6 +127,13 @@ struct sdpc_ctx {
   double* upd = nullptr;         // multifrontal update matrices
   double* Xh = nullptr;          // dense X-hat, panel-major [npanels][n][32]
   double* Yh = nullptr;          // dense Y^{-1}
+  double* Uh = nullptr;          // search direction: dense panels G Y^{-1} / dY Y^{-1}, then X-hat times them
+  double* dir_ws = nullptr;      // search direction scratch (m doubles + flags)
+  std::vector<int64_t> step_off; // primal step length: per clique offset of its 3 c x c blocks
+  int64_t* d_step_off = nullptr;
+  double* step_ws = nullptr;
+  unsigned long long* d_amin = nullptr;
+  double* ytmp = nullptr;        // dual step length: Y + alpha dY on E
   int32_t* d_err = nullptr;
   int32_t* d_ok = nullptr;       // constant kNoError flag (distributed tile kernels)
   double* Bown = nullptr;        // handle-owned B for sdpc_iteration_host
@@ -161,6 +178,7 @@ namespace sdpc {
 int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st);
 int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err = nullptr, int set = 0);
 int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0 = 0, int nfac = 2, int max_ctas = 0);
+int launch_apply_inverse(sdpc_ctx* h, cudaStream_t st, int fac, const double* in, double* out);
 int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st);
 int launch_panels_to_E(sdpc_ctx* h, const double* panels, double* E, cudaStream_t st);
 int launch_gather_columns(sdpc_ctx* h, const int32_t* d_cols_new, int32_t ncols, double* Xo, double* Yo,
@@ -173,6 +191,12 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
 // 16-byte aligned with an even ld (potrf_dag_usable).  Returns launches (-1: workspace allocation failed).
 bool potrf_dag_usable(const double* B, int64_t ld);
 int potrf_dag(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st);
+// Search direction and step lengths (k_direction.cu); each returns launches or -1.
+int direction_g(sdpc_ctx* h, const double* xbar_E, const double* G_E, double bmu, double* g, cudaStream_t st);
+int direction_dY_dX(sdpc_ctx* h, const double* xbar_E, const double* G_E, double bmu, const double* dz, double* dY_E,
+                    double* dX_E, cudaStream_t st);
+int primal_step(sdpc_ctx* h, const double* xbar_E, const double* dX_E, double* alpha_p, cudaStream_t st);
+int dual_step(sdpc_ctx* h, const double* y_E, const double* dY_E, double* alpha_d, int steps, cudaStream_t st);
 // Distributed-Cholesky tile kernels; see sdpc.h.
 int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t ldl, const double* inv, int kb,
                const int32_t* d_err, cudaStream_t st);

@@ -47,6 +47,11 @@ struct SolveArgs {
   const double* Lp[2];
   const double* D[2];
   double* out[2];
+  // general right-hand sides (P-MATRIX and g, Eq. newdX2): when rhs_in is set, panel P's input
+  // is the dense panel rhs_in[P] (same layout as out; in place allowed) instead of the identity columns
+  // e_{rhs[..]}; the forward sweep then runs over every supernode (full_sn = 0..nsuper-1)
+  const double* rhs_in;
+  const int32_t* full_sn;
 };
 
 constexpr int kSolveThreads = 256;
@@ -364,24 +369,32 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
   const double* __restrict__ D = a.D[fac];
   double* X = a.out[fac] + (size_t)P * n * kPanelW;
   const int myrhs = a.rhs[P * kPanelW + lane];  // this lane's RHS: e_{myrhs} (all-zero column if -1)
+  const bool gen = a.rhs_in != nullptr;
+  const double* Xin = gen ? a.rhs_in + (size_t)P * n * kPanelW : nullptr;
   // truncated backward (SURVEY §8(a) note): only rows i >= pmin of this panel are read later, and
   // row i of x depends only on rows > i, so supernodes entirely below pmin are skipped
-  const int pmin = a.trunc ? a.rhs[P * kPanelW] : -1;
+  const int pmin = (a.trunc && !gen) ? a.rhs[P * kPanelW] : -1;
   const int32_t* __restrict__ rowind = a.rowind;
+  const int32_t* __restrict__ reach_sn = gen ? a.full_sn : a.reach_sn;
 
   const int nwords = (a.nsuper + 31) / 32;
   for (int i = tid; i < nwords; i += kSolveThreads) inreach[i] = 0;
   __syncthreads();
-  const int rb = a.reach_ptr[P], re = a.reach_ptr[P + 1];
+  const int rb = gen ? 0 : a.reach_ptr[P], re = gen ? a.nsuper : a.reach_ptr[P + 1];
   for (int q = rb + tid; q < re; q += kSolveThreads) {
-    const int r = a.reach_sn[q];
+    const int r = reach_sn[q];
     atomicOr(&inreach[r >> 5], 1u << (r & 31));
   }
-  // initialise z rows on the paths: z[i][lane] = (i == myrhs)
+  // initialise z rows on the paths: z[i][lane] = (i == myrhs), or the given dense panel
   for (int q = rb + wid; q < re; q += NW) {
-    const int r = a.reach_sn[q];
+    const int r = reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r];
-    for (int t = 0; t < s; ++t) xrow(X, f + t, lane) = (f + t == myrhs) ? 1.0 : 0.0;
+    if (gen) {
+      if (Xin != X)
+        for (int t = 0; t < s; ++t) xrow(X, f + t, lane) = Xin[(size_t)(f + t) * kPanelW + lane];
+    } else {
+      for (int t = 0; t < s; ++t) xrow(X, f + t, lane) = (f + t == myrhs) ? 1.0 : 0.0;
+    }
   }
   __syncthreads();
 
@@ -395,7 +408,7 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
     pend_f = -1;
   };
   for (int q = rb; q < re; ++q) {
-    const int r = a.reach_sn[q];
+    const int r = reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
     const double* Lr = Lp + a.panel_off[r];
     flush(NW - 1);
@@ -421,7 +434,7 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
   __syncthreads();
   // z <- D^{-1} z on the path rows (deferred: the U updates above use the unscaled z)
   for (int q = rb + wid; q < re; q += NW) {
-    const int r = a.reach_sn[q];
+    const int r = reach_sn[q];
     const int f = a.super_ptr[r], s = a.sns[r];
     for (int t = 0; t < s; ++t) xrow(X, f + t, lane) /= D[f + t];
   }
@@ -475,7 +488,20 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
   }
 }
 
+static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int max_ctas, const double* in,
+                         double* out, bool trunc);
+
 int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int max_ctas) {
+  return launch_panels(h, st, fac0, nfac, max_ctas, nullptr, nullptr, h->trunc_active);
+}
+
+// out[P] = X-hat in[P] (factor 0) or Y^{-1} in[P] (factor 1) for every RHS panel P (in == out allowed)
+int launch_apply_inverse(sdpc_ctx* h, cudaStream_t st, int fac, const double* in, double* out) {
+  return launch_panels(h, st, fac, 1, 0, in, out, false);
+}
+
+static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int max_ctas, const double* in,
+                         double* out, bool trunc) {
   SolveArgs a{};
   a.n = h->S.n;
   a.nsuper = h->S.nsuper;
@@ -495,7 +521,7 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int 
   a.sub_ptr = h->d.sub_ptr;
   a.ntop = h->S.ntop;
   a.nsub = (int32_t)h->S.sub_ptr.size() - 1;
-  a.trunc = h->trunc_active ? 1 : 0;
+  a.trunc = trunc ? 1 : 0;
   a.sparent = h->d.sparent;
   a.Lp[0] = h->Lx;
   a.Lp[1] = h->Ly;
@@ -503,6 +529,11 @@ int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int 
   a.D[1] = h->Dy;
   a.out[0] = h->Xh;
   a.out[1] = h->Yh;
+  if (in) {
+    a.rhs_in = in;
+    a.out[fac0] = out;
+    a.full_sn = h->d.all_sn;
+  }
   size_t smem = sizeof(double) * (kChunk + 2 * kKc) * kVs + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
   static bool attr = false;
   if (!attr) {

@@ -38,6 +38,8 @@ _SIGS = [
     ("sdpc_iteration_host", C.c_int, [_P, _P, _P, _P, _P, _P]),
     ("sdpc_get_phase_times", C.c_int, [_P, _P]),
     ("sdpc_get_kernel_times", C.c_int, [_P, _P]),
+    ("sdpc_search_direction", C.c_int, [_P, _P, _P, C.c_double, _P, C.c_int64, _P, _P, _P, _P, _P]),
+    ("sdpc_step_lengths", C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     ("sdpc_set_timing", C.c_int, [_P, C.c_int32]),
     ("sdpc_set_truncation", C.c_int, [_P, C.c_int32]),
     ("sdpc_set_cholesky_schedule", C.c_int, [_P, C.c_int32]),
@@ -219,6 +221,19 @@ class Handle:
         t = (C.c_double * 8)()
         self._check(lib().sdpc_get_phase_times(self.h, t), "sdpc_get_phase_times")
         return list(t)
+
+    def search_direction(self, xbar_E, G_E, beta_mu, R, ldr, g, dz, dY_E, dX_E, stream=None):
+        """sdpc_search_direction: g, dz, dY, dX (device tensors) of the HKM direction."""
+        self._check(lib().sdpc_search_direction(self.h, _ptr(xbar_E), _ptr(G_E), float(beta_mu), _ptr(R), int(ldr),
+                                                _ptr(g), _ptr(dz), _ptr(dY_E), _ptr(dX_E), _stream(stream)),
+                    "sdpc_search_direction")
+
+    def step_lengths(self, xbar_E, dX_E, y_E, dY_E, stream=None):
+        """sdpc_step_lengths -> (alpha_p, alpha_d)."""
+        ap, ad = C.c_double(0), C.c_double(0)
+        self._check(lib().sdpc_step_lengths(self.h, _ptr(xbar_E), _ptr(dX_E), _ptr(y_E), _ptr(dY_E), C.byref(ap),
+                                            C.byref(ad), _stream(stream)), "sdpc_step_lengths")
+        return ap.value, ad.value
 
     def kernel_times(self):
         t = (C.c_double * 8)()
