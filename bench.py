@@ -36,6 +36,8 @@ CONFIG_TEXT = {
     2: "configs[2]: theta max-clique SDP, 60x60 torus, n=3600, m=7201, MD order",
     3: "configs[3]: block-arrow SDP, n=20200, m=5000, identity order",
     4: "configs[4]: max-cut SDP, 200x200 torus, n=m=40000, ND order",
+    5: "NEXT 4 (not a BASELINE config): max-cut SDP on the 18x18x18 3D torus (SpinGlass18 shape), n=m=5832, 3D ND",
+    6: "NEXT 4 (not a BASELINE config): max-cut SDP on the 25x25x25 3D torus (SpinGlass25 shape), n=m=15625, 3D ND",
 }
 # Nominal B200 ratio FP64-tensor / BF16-dense (45 / 2250 TFLOP/s, /opt/skills guides) applied to the
 # measured bf16 peak (MEASURED_PEAKS.json) -> FP64 tensor peak for the roofline.
@@ -567,7 +569,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4, 5, 6])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

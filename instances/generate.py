@@ -83,14 +83,15 @@ def _pack(mats, n):
     return ptr, rows, cols, vals
 
 
-def _maxcut_data(k: int, rng_w):
-    """Max-cut SDP on the k x k torus (configs 0, 1, 4).
+def _maxcut_data(k: int, rng_w, edges=None):
+    """Max-cut SDP on the k x k torus (configs 0, 1, 4), or on the given edge
+    list (the 3D torus of configs 5, 6; n = max id + 1).
 
     A_0 = -(1/4) * Laplacian(W) with W_e Rademacher +-1;
     A_k = e_k e_k^T, b_k = 1.
     """
-    n = k * k
-    e = graphs.torus_edges(k)
+    e = graphs.torus_edges(k) if edges is None else edges
+    n = k * k if edges is None else int(edges.max()) + 1
     w = rng_w.choice(np.array([-1.0, 1.0]), size=len(e))
     deg = np.zeros(n)
     np.add.at(deg, e[:, 0], w)
@@ -287,6 +288,10 @@ CONFIGS = {
     2: dict(kind="theta", k=60, order="md"),
     3: dict(kind="blockarrow", nblk=200, bsz=100, border=200, m=5000),
     4: dict(kind="maxcut", k=200, order="nd"),
+    # 3D spin-glass torus (Table 3 SpinGlass18 / SpinGlass25),
+    # not BASELINE configs
+    5: dict(kind="maxcut3d", p=18, order="nd3"),
+    6: dict(kind="maxcut3d", p=25, order="nd3"),
 }
 
 
@@ -296,6 +301,8 @@ def build(kind: str, seed: int = 0, name: Optional[str] = None, **kw) -> Instanc
     if kind == "maxcut":
         k = kw["k"]
         n, m, mats, b, e = _maxcut_data(k, rng_w)
+    elif kind == "maxcut3d":
+        n, m, mats, b, e = _maxcut_data(kw["p"], rng_w, graphs.torus3d_edges(kw["p"]))
     elif kind == "theta":
         k = kw["k"]
         n, m, mats, b, e = _theta_data(k, rng_w)
@@ -310,6 +317,8 @@ def build(kind: str, seed: int = 0, name: Optional[str] = None, **kw) -> Instanc
         perm = orderings.minimum_degree(n, edges)
     elif order == "nd":
         perm = orderings.torus_nested_dissection(kw["k"])
+    elif order == "nd3":
+        perm = orderings.torus3d_nested_dissection(kw["p"])
     else:
         perm = np.arange(n, dtype=np.int32)
     colptr, rowind = _symbolic(n, perm, edges)
@@ -320,7 +329,7 @@ def build(kind: str, seed: int = 0, name: Optional[str] = None, **kw) -> Instanc
     y = product_on_E(n, colptr, rowind, Ly, Dy)
     return Instance(name=name or kind, n=n, m=m, a_ptr=a_ptr, a_row=a_row, a_col=a_col,
                     a_val=a_val, b=b, perm=perm.astype(np.int32), colptr=colptr, rowind=rowind,
-                    L=L, D=D, Ly=Ly, Dy=Dy, xbar=xbar, y=y, kind=kind)
+                    L=L, D=D, Ly=Ly, Dy=Dy, xbar=xbar, y=y, kind="maxcut" if kind == "maxcut3d" else kind)
 
 
 def _cache_dir():

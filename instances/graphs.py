@@ -53,3 +53,19 @@ def block_arrow_lower_pattern(nblk: int, bsz: int, border: int):
         rows.append(rr)
         cols.append(np.full(rr.shape, j))
     return np.concatenate(rows).astype(np.int64), np.concatenate(cols).astype(np.int64), n
+
+
+def torus3d_edges(p: int) -> np.ndarray:
+    """Edges of the p x p x p toroidal lattice (6 neighbours), vertex id v = (x*p + y)*p + z: the shape of
+    the paper's 3D spin-glass set (Table 3 SpinGlass18-25).
+    Edges as (min id, max id) rows sorted lexicographically; p >= 3 gives 3 p^3 edges."""
+    if p < 3:
+        raise ValueError("torus needs p >= 3")
+    v = np.arange(p ** 3, dtype=np.int64)
+    x, rem = np.divmod(v, p * p)
+    y, z = np.divmod(rem, p)
+    nb = [((x + 1) % p * p + y) * p + z, (x * p + (y + 1) % p) * p + z, (x * p + y) * p + (z + 1) % p]
+    a = np.concatenate([v, v, v])
+    b = np.concatenate(nb)
+    e = np.stack([np.minimum(a, b), np.maximum(a, b)], axis=1)
+    return np.unique(e, axis=0)

@@ -95,3 +95,58 @@ def torus_nested_dissection(k: int) -> np.ndarray:
     perm = np.asarray(out, dtype=np.int32)
     assert perm.size == k * k and np.unique(perm).size == k * k
     return perm
+
+
+def _box(lo, hi, p, out):
+    """Geometric ND of the open box [lo, hi) (3 dims): split the longest side at its middle plane,
+    order both halves, then the plane (lexicographic x, y, z)."""
+    ext = [hi[d] - lo[d] for d in range(3)]
+    if min(ext) <= 0:
+        return
+    if ext[0] * ext[1] * ext[2] <= 8:
+        for x in range(lo[0], hi[0]):
+            for y in range(lo[1], hi[1]):
+                for z in range(lo[2], hi[2]):
+                    out.append((x * p + y) * p + z)
+        return
+    d = int(np.argmax(ext))
+    mid = (lo[d] + hi[d]) // 2
+    h1, l2 = list(hi), list(lo)
+    h1[d] = mid
+    l2[d] = mid + 1
+    _box(lo, h1, p, out)
+    _box(l2, hi, p, out)
+    pl, ph = list(lo), list(hi)
+    pl[d], ph[d] = mid, mid + 1
+    for x in range(pl[0], ph[0]):
+        for y in range(pl[1], ph[1]):
+            for z in range(pl[2], ph[2]):
+                out.append((x * p + y) * p + z)
+
+
+def torus3d_nested_dissection(p: int) -> np.ndarray:
+    """Geometric ND of the p x p x p torus (the 3D analogue of the 2D rule of SURVEY §8(d)):
+    the top separator is the six planes x, y, z in {0, p/2}, ordered last (x-planes, then y-planes minus
+    what is already taken, then z-planes); before it the eight open octants [1, h) or [h+1, p) per axis,
+    each ordered by recursive bisection of its longest side."""
+    h = p // 2
+    out: list[int] = []
+    for ox in ((1, h), (h + 1, p)):
+        for oy in ((1, h), (h + 1, p)):
+            for oz in ((1, h), (h + 1, p)):
+                _box([ox[0], oy[0], oz[0]], [ox[1], oy[1], oz[1]], p, out)
+    seen = np.zeros(p ** 3, dtype=bool)
+    seen[out] = True
+    for d in range(3):
+        for c in (0, h):
+            for a in range(p):
+                for b in range(p):
+                    xyz = [a, b]
+                    xyz.insert(d, c)
+                    v = (xyz[0] * p + xyz[1]) * p + xyz[2]
+                    if not seen[v]:
+                        seen[v] = True
+                        out.append(v)
+    perm = np.asarray(out, dtype=np.int32)
+    assert perm.size == p ** 3 and np.unique(perm).size == p ** 3
+    return perm

@@ -76,6 +76,8 @@ def small(kind, seed=0):
         return build("theta", seed=seed, k=5, order="md", name="theta5")
     if kind == "blockarrow":
         return build("blockarrow", seed=seed, nblk=4, bsz=6, border=3, m=40, name="blockarrow4x6")
+    if kind == "maxcut3d":
+        return build("maxcut3d", seed=seed, p=6, order="nd3", name="maxcut3d6")
     raise ValueError(kind)
 
 

@@ -112,7 +112,7 @@ def test_3x3_worked_example():
             np.testing.assert_allclose(g["R"], gold["R_maxcut"].reshape(3, 3), atol=1e-14)
 
 
-@pytest.mark.parametrize("kind", ["maxcut_md", "maxcut_nd", "theta", "blockarrow"])
+@pytest.mark.parametrize("kind", ["maxcut_md", "maxcut_nd", "theta", "blockarrow", "maxcut3d"])
 def test_small_instances(kind):
     inst = small(kind)
     check_all(inst, run_gpu(inst), oracle_dense(inst))
@@ -236,7 +236,7 @@ def _sampled(inst, seed=1, nsample=1000):
     return sorted(cols)
 
 
-@pytest.mark.parametrize("cfg", [1, 3, 4])
+@pytest.mark.parametrize("cfg", [1, 3, 4, 5])
 def test_full_config_sampled_columns(cfg):
     """configs[1], [3], [4] at full size: >= 1000 sampled columns of B, plus free checks."""
     from instances import gen_config

@@ -205,7 +205,7 @@ def test_maxdet_optimality(kind):
             assert np.linalg.slogdet(P)[1] < base
 
 
-@pytest.mark.parametrize("kind", ["maxcut_md", "maxcut_nd", "theta", "blockarrow"])
+@pytest.mark.parametrize("kind", ["maxcut_md", "maxcut_nd", "theta", "blockarrow", "maxcut3d"])
 def test_symbolic_matches_generator_and_invariants(kind):
     inst = small(kind)
     S = _S(inst)
@@ -352,3 +352,19 @@ def test_sce_solve_worked_example_and_residual():
     assert np.linalg.norm(B @ X - Rhs) / np.linalg.norm(Rhs) < 1e-13
     for q in range(3):
         np.testing.assert_allclose(CHO.sce_solve(B, Rhs[:, q]), X[:, q], rtol=1e-12, atol=1e-14)
+
+
+def test_torus3d_workload_shape():
+    """NEXT 4: the 3D torus has n = p^3 vertices of degree 6 (3 p^3 edges); the 3D geometric
+    ND is a permutation whose E is chordal with the oracle's elimination game."""
+    from instances import graphs, orderings
+    for p in (4, 5, 6):
+        e = graphs.torus3d_edges(p)
+        assert e.shape == (3 * p ** 3, 2)
+        deg = np.bincount(e.ravel(), minlength=p ** 3)
+        assert np.all(deg == 6)
+        perm = orderings.torus3d_nested_dissection(p)
+        assert np.array_equal(np.sort(perm), np.arange(p ** 3))
+    inst = small("maxcut3d")
+    S = _S(inst)
+    assert np.array_equal(S.colptr, inst.colptr) and np.array_equal(S.rowind, inst.rowind)
