@@ -325,9 +325,11 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_ours_dist(args, rank, world, local_rank):
-    """N > 1: one problem over N GPUs (strong scaling).  Each rank builds its 2D block-cyclic tiles of
-    B (sdpc_scm_build with nranks = N) and the ranks factor B with the distributed schedule of
-    paper_1310_6919_b200/dist.py (NCCL broadcasts / all-gathers through torch.distributed)."""
+    """N > 1: one problem over N GPUs (strong scaling).  Each rank builds its 2D block-cyclic tiles of B
+    (sdpc_scm_build with nranks = N) and the ranks factor B collectively inside the library
+    (sdpc_scm_cholesky over the handle's NCCL communicators, created by sdpc_create from the 128-byte id
+    of sdpc_get_unique_id that torch.distributed broadcasts).  SDPC_BENCH_BACKEND=gloo (test hook, ranks
+    sharing one GPU) keeps the host-driven schedule of paper_1310_6919_b200/dist.py instead."""
     import numpy as np
     import torch
 
@@ -336,28 +338,40 @@ def run_ours_dist(args, rank, world, local_rank):
 
     __graft_entry__.build()
     from paper_1310_6919_b200 import Handle, dist as D
+    from paper_1310_6919_b200.sdpc import get_unique_id
 
     dev = torch.device("cuda", local_rank)
     inst = gen_config(args.config, seed=args.seed)
     n, m = inst.n, inst.m
-    h = Handle.from_instance(inst, device=local_rank, nranks=world, rank=rank)
+    dist = torch.distributed
+    via_lib = os.environ.get("SDPC_BENCH_BACKEND", "nccl") == "nccl"
+    uid = None
+    if via_lib:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, src=0)
+        uid = bytes(idt.cpu().numpy().tobytes())
+    h = Handle.from_instance(inst, device=local_rank, nranks=world, rank=rank, nccl_id=uid)
     L = D.Layout(m, world, rank)
     lay = h.get_scm_layout()
     assert (lay["mloc"], lay["nloc"]) == (L.mloc, L.nloc)
-    comm = D.TorchComm(L)
+    comm = None if via_lib else D.TorchComm(L)
     x = torch.from_numpy(inst.xbar).to(dev)
     y = torch.from_numpy(inst.y).to(dev)
     Bt = torch.empty((max(1, L.nloc), L.lld), dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
-    dist = torch.distributed
 
     def step(timer=None, tb=None):
         h.factor_xinv(x, stream)
         h.scm_build(y, Bt, L.lld, stream)
         if tb is not None:
             tb.record(stream)
-        info = D.dist_cholesky(h, Bt, L, comm, dev, stream, timer=timer)
+        if via_lib:
+            info = h.scm_cholesky(Bt, L.lld, stream)
+        else:
+            info = D.dist_cholesky(h, Bt, L, comm, dev, stream, timer=timer)
         assert info == 0, info
 
     for _ in range(args.warmup):
@@ -405,10 +419,19 @@ def run_ours_dist(args, rank, world, local_rank):
     if rank != 0:
         return None
     pk = peaks()
-    fp64_peak_tf = pk["bf16_sus"] * FP64_OVER_BF16
-    upd_ms = statistics.mean(u[0] for u in upd)
-    upd_fl = statistics.mean(u[1] for u in upd)
+    from paper_1310_6919_b200 import fp64_peak
+    dmma = fp64_peak(local_rank, 1500.0)[0] if args.measure_peak else None
+    fp64_peak_tf = max(pk["bf16_sus"] * FP64_OVER_BF16, dmma or 0.0)
+    if via_lib:
+        # the whole distributed Cholesky (one library call per rank): m^3/3 over the max-rank time,
+        # against world x the per-GPU FP64 roof
+        upd_ms = ms - build_ms
+        upd_fl = m ** 3 / 3.0
+    else:
+        upd_ms = statistics.mean(u[0] for u in upd)
+        upd_fl = statistics.mean(u[1] for u in upd)
     achieved = upd_fl / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else None
+    peak_all = fp64_peak_tf * (world if via_lib else 1)
     return {
         "metric": METRIC, "value": entries(m) / (ms * 1e-3), "unit": "B-entries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "s_per_iter": ms * 1e-3,
@@ -421,15 +444,17 @@ def run_ours_dist(args, rank, world, local_rank):
                       "rank0_update_kernels": upd_ms},
         "clocks": clk.summary(),
         "gpu_launches": int(launches), "gpu_launches_per_step": launches / args.steps,
-        "roofline": {"kernel": "gemm_nt_kernel<DIST> (rank 0 local trailing updates, DMMA)", "bound": "tensor",
-                     "achieved": achieved, "peak": fp64_peak_tf, "unit": "TFLOP/s",
-                     "frac": (achieved / fp64_peak_tf) if achieved else None, "traffic": None,
-                     "peak_source": f"{pk['src']} bf16 sustained {pk['bf16_sus']} x FP64/BF16 nominal 45/2250",
-                     "launches_per_step": upd[0][2] if upd else 0, "flops_per_step": upd_fl},
+        "roofline": {"kernel": ("sdpc_scm_cholesky over NCCL (2D block-cyclic, all ranks; DMMA tile kernels)"
+                                if via_lib else "gemm_nt_kernel<DIST> (rank 0 local trailing updates, DMMA)"),
+                     "bound": "tensor", "achieved": achieved, "peak": peak_all, "unit": "TFLOP/s",
+                     "frac": (achieved / peak_all) if achieved else None, "traffic": None,
+                     "peak_source": (f"{world} x per-GPU FP64 roof {fp64_peak_tf:.1f} TF/s (builder-measured DMMA "
+                                     f"microbenchmark when available, else {pk['src']} bf16 sustained x 45/2250)"),
+                     "launches_per_step": upd[0][2] if upd else 1, "flops_per_step": upd_fl},
         "e2e": {"value": entries(m) / (e2e_ms * 1e-3), "unit": "B-entries/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(2 * 8 * inst.nnzE), "d2h_bytes_per_step": 4,
                 "api": "per rank: pinned host xbar_E, y_E -> device, sdpc_factor_xinv + sdpc_scm_build + "
-                       "distributed Cholesky, info to host"},
+                       "sdpc_scm_cholesky (collective over NCCL), info to host"},
     }
 
 

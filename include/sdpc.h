@@ -95,16 +95,25 @@ typedef struct {
  *                 rank builds exactly its own tiles of B (columns l with (l/256) mod Pc == mycol
  *                 need the RHS x_p, y_q of A_l only, Eq. newSCM2: columns of B are
  *                 independent); (a1)/(a2) are replicated.  The library holds no
- *                 communicator: the caller moves tiles between ranks (torch.distributed / NCCL)
- *                 around the tile entries below.
- *   nccl_id     : reserved, must be NULL.
+ *                 communicator unless created with an NCCL id (see nccl_id).
+ *   nccl_id     : NULL, or the 128-byte NCCL unique id from sdpc_get_unique_id on one rank, shipped to
+ *                 every rank by the caller (e.g. a torch.distributed broadcast).  With an id, the
+ *                 nranks callers create collectively an NCCL world communicator plus process-row and
+ *                 process-column communicators owned by the handle, and sdpc_scm_cholesky factors the
+ *                 distributed B collectively.  Without one (nranks > 1), the caller drives the tile
+ *                 entries below, or sdpc_scm_cholesky_virtual on one device.
  * Host arrays are copied.  Errors: INVALID_ARG (sizes, out-of-range ids, row < col,
- * perm not a permutation, rank outside [0, nranks)), OOM, CUDA (no device / not sm_100).
+ * perm not a permutation, rank outside [0, nranks)), OOM, CUDA (no device / not sm_100),
+ * NCCL (communicator creation failed; message in sdpc_last_error_message).
  */
 sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m,
                         const int64_t* a_ptr, const int32_t* a_row, const int32_t* a_col,
                         const double* a_val, const double* b, const int32_t* perm,
                         int32_t device, int32_t nranks, int32_t rank, const void* nccl_id);
+
+/* The 128-byte NCCL unique id for sdpc_create's nccl_id (call on one rank, broadcast to all).  NCCL is
+ * loaded at run time (libnccl.so.2, or the path in SDPC_NCCL_LIB).  Errors: NCCL. */
+sdpc_status sdpc_get_unique_id(void* id_out);
 
 sdpc_status sdpc_get_structure(sdpc_handle h, sdpc_structure* out);
 sdpc_status sdpc_get_scm_layout(sdpc_handle h, sdpc_layout* out);
@@ -178,9 +187,24 @@ sdpc_status sdpc_get_inverse_columns(sdpc_handle h, const int32_t* cols, int32_t
  * sdpc_scm_cholesky - (d) in place: lower(B) <- R with B = R R^T (LAPACK potrf 'L' rule).
  *   info (HOST): 0 on success; k > 0 if the leading minor of order k is not positive
  *   definite (pivot <= 0 or NaN), in which case status = NOT_PD and last_info = k.
- * nranks > 1: B is the local 2D block-cyclic buffer; the factorization is collective.
+ * Handle created with an NCCL id: B is this rank's local 2D block-cyclic array (mloc x nloc, ldb >= lld)
+ *   and the call is collective over the nranks processes: right-looking 256-tile steps (tile potrf on
+ *   the owner, broadcast down the process column, panel trsm, the live panel slice broadcast along process
+ *   rows and all-gathered in process columns, local DMMA trailing updates with depth-1 lookahead; row (e),
+ *   SURVEY §8(e)).  info is the smallest failing global column, identical on every rank.
+ * nranks > 1 without a communicator: STATE.
  */
 sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream);
+
+/*
+ * sdpc_scm_cholesky_virtual - the same distributed factorisation with every rank of the grid in this
+ * process on one device (test transport: hs[r] = the handle of rank r, created with nranks and no NCCL
+ * id; B[r] its local array): the host runs each rank's part of every step in turn on `stream` and the
+ * collectives are device copies between the ranks' buffers (no rank waits on another inside a kernel).
+ * info and status as for sdpc_scm_cholesky (set on every handle).
+ */
+sdpc_status sdpc_scm_cholesky_virtual(const sdpc_handle* hs, int32_t nranks, double* const* B, int64_t ldb,
+                                      int32_t* info, void* stream);
 
 /*
  * sdpc_scm_solve - the Schur complement equation (SCE) of the search direction, B dz = g

@@ -134,7 +134,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     if (!std::isfinite(b[k])) return SDPC_ERR_INVALID_ARG;
   for (int64_t e = 0; e < a_ptr[m + 1]; ++e)
     if (!std::isfinite(a_val[e])) return SDPC_ERR_INVALID_ARG;
-  if (nranks < 1 || rank < 0 || rank >= nranks || nccl_id != nullptr) return SDPC_ERR_INVALID_ARG;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return SDPC_ERR_INVALID_ARG;
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return SDPC_ERR_CUDA;
@@ -505,13 +505,29 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
       cudaMemset(h->d_ok, 0x7f, sizeof(int32_t)) != cudaSuccess)
     return fail(SDPC_ERR_CUDA);
   if (cudaGetLastError() != cudaSuccess) return fail(SDPC_ERR_CUDA);
+  if (nccl_id) {
+    // NCCL world + process-row / process-column communicators (collective over the nranks callers)
+    std::string why;
+    if (nccl_init(h, nccl_id, &why) != 0) {
+      h->err = why;
+      return fail(SDPC_ERR_NCCL);
+    }
+  }
   *out = h;
   return SDPC_OK;
+}
+
+sdpc_status sdpc_get_unique_id(void* id_out) {
+  if (!id_out) return SDPC_ERR_INVALID_ARG;
+  std::string why;
+  return nccl_unique_id(id_out, &why) == 0 ? SDPC_OK : SDPC_ERR_NCCL;
 }
 
 sdpc_status sdpc_destroy(sdpc_handle h) {
   if (!h) return SDPC_OK;
   cudaSetDevice(h->device);
+  nccl_destroy(h);
+  if (h->dist_side) cudaStreamDestroy(h->dist_side);
   DevSym& d = h->d;
   void* ptrs[] = {d.colptr, d.rowind, d.super_ptr, d.snc, d.sns, d.sparent, d.panel_off, d.e2p, d.umap_off,
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
@@ -765,9 +781,31 @@ static cudaError_t run_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* 
   return cudaGetLastError();
 }
 
+static sdpc_status dist_status(sdpc_handle h, int rc, int64_t v, const std::string& why, int32_t* info) {
+  if (rc != 0) {
+    h->err = why;
+    return SDPC_ERR_NCCL;
+  }
+  *info = (int32_t)v;
+  h->last_info = v;
+  return v ? SDPC_ERR_NOT_PD : SDPC_OK;
+}
+
 sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* info, void* stream) {
-  if (!h || !B || !info || ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
-  if (h->nranks != 1) return SDPC_ERR_STATE;  // distributed: sdpc_potrf_tile / trsm_panel / update_tiles
+  if (!h || !B || !info) return SDPC_ERR_INVALID_ARG;
+  if (h->nccl_world) {
+    // collective over the handle's NCCL communicator: B is this rank's local 2D block-cyclic array
+    if (ldb < std::max<int64_t>(1, h->mloc)) return SDPC_ERR_INVALID_ARG;
+    CK(cudaSetDevice(h->device));
+    std::string why;
+    int64_t v = 0;
+    double* Bs[1] = {B};
+    sdpc_ctx* hs[1] = {h};
+    const int rc = dist_cholesky_handles(hs, Bs, ldb, 1, false, (cudaStream_t)stream, &v, &why);
+    return dist_status(h, rc, v, why, info);
+  }
+  if (h->nranks != 1) return SDPC_ERR_STATE;  // distributed without a communicator: the tile entries
+  if (ldb < h->S.m) return SDPC_ERR_INVALID_ARG;
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   CK(cudaMemsetAsync(h->d_err, 0x7f, sizeof(int32_t), st));
@@ -794,6 +832,25 @@ sdpc_status sdpc_scm_cholesky(sdpc_handle h, double* B, int64_t ldb, int32_t* in
   }
   *info = 0;
   return SDPC_OK;
+}
+
+sdpc_status sdpc_scm_cholesky_virtual(const sdpc_handle* hs, int32_t nranks, double* const* B, int64_t ldb,
+                                      int32_t* info, void* stream) {
+  if (!hs || !B || !info || nranks < 1) return SDPC_ERR_INVALID_ARG;
+  for (int32_t r = 0; r < nranks; ++r) {
+    if (!hs[r] || !B[r] || hs[r]->nranks != nranks || hs[r]->rank != r || hs[r]->device != hs[0]->device ||
+        hs[r]->S.m != hs[0]->S.m || ldb < std::max<int64_t>(1, hs[r]->mloc))
+      return SDPC_ERR_INVALID_ARG;
+  }
+  sdpc_handle h = hs[0];
+  CK(cudaSetDevice(h->device));
+  std::string why;
+  int64_t v = 0;
+  std::vector<sdpc_ctx*> hv(hs, hs + nranks);
+  const int rc = dist_cholesky_handles(hv.data(), B, ldb, nranks, true, (cudaStream_t)stream, &v, &why);
+  sdpc_status s = SDPC_OK;
+  for (int32_t r = 0; r < nranks; ++r) s = dist_status(hs[r], rc, v, why, info);
+  return s;
 }
 
 sdpc_status sdpc_iteration(sdpc_handle h, const double* xbar_E, const double* y_E, double* B, int64_t ldb,

@@ -152,6 +152,10 @@ struct sdpc_ctx {
   unsigned long long* dag_trace = nullptr;  // optional per-task trace (sdpc_set_cholesky_trace)
   int64_t dag_trace_cap = 0;
   cudaStream_t st2 = nullptr;    // lookahead stream of the SCM Cholesky
+  void* nccl_world = nullptr;    // ncclComm_t (sdpc_create with an NCCL id): world, process row, process column
+  void* nccl_row = nullptr;
+  void* nccl_col = nullptr;
+  cudaStream_t dist_side = nullptr;  // side stream of the distributed Cholesky's bulk updates
   cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // = sides[0]: (a1) size classes
   cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaStream_t sides[2][4] = {};   // [0]: (a1) / (a2) size classes, [1]: (a2) inside sdpc_iteration
@@ -197,6 +201,12 @@ int direction_dY_dX(sdpc_ctx* h, const double* xbar_E, const double* G_E, double
                     double* dX_E, cudaStream_t st);
 int primal_step(sdpc_ctx* h, const double* xbar_E, const double* dX_E, double* alpha_p, cudaStream_t st);
 int dual_step(sdpc_ctx* h, const double* y_E, const double* dY_E, double* alpha_d, int steps, cudaStream_t st);
+// NCCL (dist_chol.cu, loaded with dlopen) and the distributed SCM Cholesky behind sdpc_scm_cholesky.
+int nccl_unique_id(void* out, std::string* why);
+int nccl_init(sdpc_ctx* h, const void* id, std::string* why);
+void nccl_destroy(sdpc_ctx* h);
+int dist_cholesky_handles(sdpc_ctx* const* hs, double* const* B, int64_t ld, int nloc_ranks, bool virt,
+                          cudaStream_t st, int64_t* info, std::string* why);
 // Distributed-Cholesky tile kernels; see sdpc.h.
 int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t ldl, const double* inv, int kb,
                const int32_t* d_err, cudaStream_t st);

@@ -21,6 +21,7 @@ _P = C.c_void_p
 _SIGS = [
     ("sdpc_create", C.c_int, [C.POINTER(_P), C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
                               C.c_int32, _P]),
+    ("sdpc_get_unique_id", C.c_int, [_P]),
     ("sdpc_get_structure", C.c_int, [_P, _P]),
     ("sdpc_get_scm_layout", C.c_int, [_P, _P]),
     ("sdpc_factor_xinv", C.c_int, [_P, _P, _P]),
@@ -30,6 +31,7 @@ _SIGS = [
     ("sdpc_get_inverse_columns", C.c_int, [_P, _P, C.c_int32, _P, _P, _P]),
     ("sdpc_scm_cholesky", C.c_int, [_P, _P, C.c_int64, _P, _P]),
     ("sdpc_scm_solve", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, _P]),
+    ("sdpc_scm_cholesky_virtual", C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P]),
     ("sdpc_potrf_tile", C.c_int, [_P, _P, C.c_int32, C.c_int64, _P, _P, _P]),
     ("sdpc_trsm_panel", C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_int32, _P]),
     ("sdpc_update_tiles", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
@@ -117,8 +119,12 @@ class Handle:
                       np.ascontiguousarray(b, dtype=np.float64)]
         pp = None if perm is None else np.ascontiguousarray(perm, dtype=np.int32)
         h = _P()
+        nid = None
+        if nccl_id is not None:
+            self._nid = (C.c_char * 128).from_buffer_copy(bytes(nccl_id))
+            nid = C.addressof(self._nid)
         st = L.sdpc_create(C.byref(h), int(n), int(m), *[_ptr(x) for x in self._keep], _ptr(pp), int(device),
-                           int(nranks), int(rank), nccl_id)
+                           int(nranks), int(rank), nid)
         if st != SDPC_OK:
             raise SdpcError(st, 0, "sdpc_create")
         self.h = h
@@ -126,9 +132,9 @@ class Handle:
         self.device = device
 
     @classmethod
-    def from_instance(cls, inst, device=0, with_perm=True, nranks=1, rank=0):
+    def from_instance(cls, inst, device=0, with_perm=True, nranks=1, rank=0, nccl_id=None):
         return cls(inst.n, inst.m, inst.a_ptr, inst.a_row, inst.a_col, inst.a_val, inst.b,
-                   inst.perm if with_perm else None, device, nranks, rank)
+                   inst.perm if with_perm else None, device, nranks, rank, nccl_id)
 
     def _check(self, st, where):
         if st != SDPC_OK:
@@ -274,6 +280,30 @@ class Handle:
             self.destroy()
         except Exception:
             pass
+
+
+def get_unique_id():
+    """sdpc_get_unique_id: the 128-byte NCCL id (bytes) for Handle(..., nccl_id=...)."""
+    buf = (C.c_char * 128)()
+    st = lib().sdpc_get_unique_id(buf)
+    if st != SDPC_OK:
+        raise SdpcError(st, 0, "sdpc_get_unique_id")
+    return bytes(buf)
+
+
+def scm_cholesky_virtual(handles, Bs, ldb, stream=None):
+    """sdpc_scm_cholesky_virtual: the distributed Cholesky with every rank's handle in this process
+    (one device).  Returns info."""
+    P = len(handles)
+    hs = (_P * P)(*[h.h for h in handles])
+    bp = (_P * P)(*[_ptr(b) for b in Bs])
+    info = C.c_int32(0)
+    st = lib().sdpc_scm_cholesky_virtual(hs, P, bp, int(ldb), C.byref(info), _stream(stream))
+    if st == SDPC_ERR_NOT_PD:
+        return int(info.value)
+    if st != SDPC_OK:
+        raise SdpcError(st, 0, "sdpc_scm_cholesky_virtual [" + lib().sdpc_last_error_message(handles[0].h).decode() + "]")
+    return int(info.value)
 
 
 def fp64_peak(device=0, ms=2000.0):
