@@ -332,6 +332,16 @@ def build(kind: str, seed: int = 0, name: Optional[str] = None, **kw) -> Instanc
                     L=L, D=D, Ly=Ly, Dy=Dy, xbar=xbar, y=y, kind="maxcut" if kind == "maxcut3d" else kind)
 
 
+def _source_tag() -> str:
+    """Hash of the generator's own sources: a change to the recipe never reuses a stale cached instance."""
+    here = os.path.dirname(os.path.abspath(__file__))
+    h = hashlib.sha256()
+    for f in ("generate.py", "graphs.py", "orderings.py"):
+        with open(os.path.join(here, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _cache_dir():
     d = os.environ.get("SDPC_INSTANCE_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "sdpc_instances"))
     return d
@@ -341,7 +351,7 @@ def gen_config(i: int, seed: int = 0, cache: bool = True) -> Instance:
     """Instance for BASELINE.json configs[i]."""
     kw = dict(CONFIGS[i])
     kind = kw.pop("kind")
-    path = os.path.join(_cache_dir(), f"config{i}_seed{seed}_v1.npz")
+    path = os.path.join(_cache_dir(), f"config{i}_seed{seed}_{_source_tag()}.npz")
     if cache and os.path.exists(path):
         try:
             z = np.load(path, allow_pickle=False)

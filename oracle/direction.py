@@ -67,10 +67,25 @@ def inner(A, M):
     return float(np.sum(A * M))
 
 
+def _entries(inst, k):
+    """Stored lower triplets of A_k (k = 1..m), symmetric-expanded: (i, j, a) with both orientations."""
+    lo, hi = inst.a_ptr[k], inst.a_ptr[k + 1]
+    r = inst.a_row[lo:hi].astype(np.int64)
+    c = inst.a_col[lo:hi].astype(np.int64)
+    v = inst.a_val[lo:hi]
+    off = r != c
+    return np.concatenate([r, c[off]]), np.concatenate([c, r[off]]), np.concatenate([v, v[off]])
+
+
 def g_vector(inst, Xh, Yi, G, bmu):
-    """g_k = A_k . (beta mu Y^{-1} - X-hat - X-hat G Y^{-1}), k = 1..m."""
+    """g_k = A_k . (beta mu Y^{-1} - X-hat - X-hat G Y^{-1}), k = 1..m, with
+    A_k . M = sum_ij [A_k]_ij M_ij summed over the stored entries of A_k."""
     M = bmu * Yi - Xh - Xh @ G @ Yi
-    return np.array([inner(constraint_dense(inst, k), M) for k in range(1, inst.m + 1)])
+    g = np.empty(inst.m)
+    for k in range(1, inst.m + 1):
+        i, j, a = _entries(inst, k)
+        g[k - 1] = float(np.sum(a * M[i, j]))
+    return g
 
 
 def sce(B, g):
@@ -81,10 +96,11 @@ def sce(B, g):
 
 
 def dY_dense(inst, G, dz):
-    """dY = G - sum_k A_k dz_k."""
+    """dY = G - sum_k A_k dz_k, subtracting dz_k [A_k]_ij at the stored entries of A_k."""
     dY = G.copy()
     for k in range(1, inst.m + 1):
-        dY -= dz[k - 1] * constraint_dense(inst, k)
+        i, j, a = _entries(inst, k)
+        np.subtract.at(dY, (i, j), dz[k - 1] * a)
     return dY
 
 

@@ -196,7 +196,8 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   const int nh = (int)S.hlev_ptr.size() - 1;
   h->a2lev.resize(nh);
   // (a2) fronts in the global workspace with many children: their extend-add runs beforehand as a
-  // grid-wide kernel (one CTA per child, FP64 atomics) instead of inside the front's own CTA
+  // grid-wide kernel (CTAs own column ranges of the front, children added in a fixed order: no atomics)
+  // instead of inside the front's own CTA
   std::vector<uint8_t> pre(ns, 0);
   std::vector<int32_t> pre_ptr(nh + 1, 0), pre_child, pre_parent, zero_ptr(nh + 1, 0), zero_list;
   for (int lv = 0; lv < nh; ++lv) {
@@ -405,6 +406,11 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   h->cons.nvmax = nvmax;
   h->cons.ndiag = (int32_t)dlist.size();
 
+  if (!solve_smem_fits(ns)) {
+    // the solve kernel keeps a reach bitmap of the supernodes in shared memory (see k_solve.cu)
+    h->err = "too many supernodes for the solve kernel's shared-memory reach bitmap";
+    return fail(SDPC_ERR_INVALID_ARG);
+  }
   // ---- upload
   DevSym& d = h->d;
   d.n = n;
@@ -1027,7 +1033,12 @@ sdpc_status sdpc_scm_solve(sdpc_handle h, const double* R, int64_t ldr, double* 
     CK(dalloc(&h->sce_ws, (size_t)nrhs * 128));
     h->sce_cap = nrhs;
   }
-  h->launches += scm_solve(R, ldr, h->S.m, G, ldg, nrhs, h->sce_ws, st);
+  const int ls = scm_solve(R, ldr, h->S.m, G, ldg, nrhs, h->sce_ws, st);
+  if (ls < 0) {
+    h->err = "cooperative launch of the SCE solve failed";
+    return SDPC_ERR_CUDA;
+  }
+  h->launches += ls;
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
   return SDPC_OK;
@@ -1057,7 +1068,12 @@ sdpc_status sdpc_search_direction(sdpc_handle h, const double* xbar_E, const dou
     h->sce_cap = 1;
   }
   CK(cudaMemcpyAsync(dz, g, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
-  h->launches += scm_solve(R, ldr, m, dz, m, 1, h->sce_ws, st);  // B dz = g (Eq. SCE)
+  const int ls = scm_solve(R, ldr, m, dz, m, 1, h->sce_ws, st);  // B dz = g (Eq. SCE)
+  if (ls < 0) {
+    h->err = "cooperative launch of the SCE solve failed";
+    return SDPC_ERR_CUDA;
+  }
+  h->launches += ls;
   if (h->timing) CK(cudaEventRecord(h->ev[13], st));
   l = direction_dY_dX(h, xbar_E, G_E, beta_mu, dz, dY_E, dX_E, st);
   if (l < 0) return SDPC_ERR_OOM;

@@ -1,10 +1,20 @@
 // Shared device/host helpers for libsdpc kernels (sm_100a).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 
 namespace sdpc {
+
+// True the first time it is called for the current device with this flag set (kernel attributes such as
+// the dynamic shared-memory opt-in are per device: a handle on a second GPU must set them again).
+inline bool once_per_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 constexpr int kWarp = 32;
 constexpr int kPanelW = 32;  // RHS panel width of the multi-RHS solves: lane <-> RHS column

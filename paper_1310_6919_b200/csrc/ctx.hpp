@@ -183,6 +183,7 @@ int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st);
 int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err = nullptr, int set = 0);
 int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0 = 0, int nfac = 2, int max_ctas = 0);
 int launch_apply_inverse(sdpc_ctx* h, cudaStream_t st, int fac, const double* in, double* out);
+bool solve_smem_fits(int64_t nsuper);
 int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st);
 int launch_panels_to_E(sdpc_ctx* h, const double* panels, double* E, cudaStream_t st);
 int launch_gather_columns(sdpc_ctx* h, const int32_t* d_cols_new, int32_t ncols, double* Xo, double* Yo,

@@ -358,38 +358,21 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
     else F[idx] = yv;
   }
   __syncthreads();
-  // extend-add of the children's update matrices.  Two children or fewer: one child at a time (warp
-  // per column, deterministic order).  More (e.g. the block-arrow border front with 200 children):
-  // all (child, column) pairs at once with FP64 atomic adds (summation order then varies, reading #13)
+  // extend-add of the children's update matrices, one child at a time in a fixed order (warp per
+  // column; the columns of one child map to distinct columns of F): deterministic summation order, so
+  // L_Y, D_Y and B are bitwise reproducible
   {
     const int c0 = pre ? 0 : a.child_ptr[r], c1 = pre ? 0 : a.child_ptr[r + 1];
     const int lane = tid & 31, wid = tid >> 5;
-    if (c1 - c0 <= 2) {
-      for (int q = c0; q < c1; ++q) {
-        const int ch = a.child_list[q];
-        const int uc = a.snc[ch] - a.sns[ch];
-        const int32_t* rel = a.relind + a.relind_off[ch];
-        const double* Uc = a.upd + a.upd_off[ch];
-        for (int ib = wid; ib < uc; ib += NT / 32) {
-          double* Fc = F + (size_t)rel[ib] * c;
-          const double* Ucol = Uc + (size_t)ib * uc;
-          for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
-        }
-        __syncthreads();
-      }
-    } else {
-      int base = 0;
-      for (int q = c0; q < c1; ++q) {  // flat (child, column) work list, one warp per item
-        const int ch = a.child_list[q];
-        const int uc = a.snc[ch] - a.sns[ch];
-        const int32_t* rel = a.relind + a.relind_off[ch];
-        const double* Uc = a.upd + a.upd_off[ch];
-        for (int ib = (wid - base % (NT / 32) + NT / 32) % (NT / 32); ib < uc; ib += NT / 32) {
-          double* Fc = F + (size_t)rel[ib] * c;
-          const double* Ucol = Uc + (size_t)ib * uc;
-          for (int ia = ib + lane; ia < uc; ia += 32) atomicAdd(Fc + rel[ia], Ucol[ia]);
-        }
-        base += uc;
+    for (int q = c0; q < c1; ++q) {
+      const int ch = a.child_list[q];
+      const int uc = a.snc[ch] - a.sns[ch];
+      const int32_t* rel = a.relind + a.relind_off[ch];
+      const double* Uc = a.upd + a.upd_off[ch];
+      for (int ib = wid; ib < uc; ib += NT / 32) {
+        double* Fc = F + (size_t)rel[ib] * c;
+        const double* Ucol = Uc + (size_t)ib * uc;
+        for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
       }
       __syncthreads();
     }
@@ -421,29 +404,37 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
   }
 }
 
-// (a2) pre-pass for global fronts with many children: zero the front, then one CTA per child adds
-// its update matrix (lower triangle, warp per column) with FP64 atomics
-__global__ void zero_fronts_kernel(const int32_t* __restrict__ list, const int64_t* __restrict__ ws_off,
-                                   const int32_t* __restrict__ snc, double* ws) {
+// (a2) pre-pass for global fronts with many children (the block-arrow border front has 200): CTA (front,
+// q) zeroes the front's columns of chunk q and adds, child by child in a fixed order, the children's
+// update columns that land there (warp per column, distinct columns within a child, a barrier between
+// children).  Columns are owned by one CTA: no atomics, deterministic summation order.
+constexpr int kPreChunks = 8;
+__global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
   const int r = list[blockIdx.x];
-  const int64_t c = snc[r];
-  double* F = ws + ws_off[r];
-  for (int64_t i = threadIdx.x; i < c * c; i += blockDim.x) F[i] = 0.0;
-}
-
-__global__ void __launch_bounds__(256) extend_add_kernel(CliqueArgs a, const int32_t* __restrict__ child,
-                                                         const int32_t* __restrict__ parent) {
-  const int ch = child[blockIdx.x], r = parent[blockIdx.x];
   const int c = a.snc[r];
   double* F = a.ws + a.ws_off[r];
-  const int uc = a.snc[ch] - a.sns[ch];
-  const int32_t* rel = a.relind + a.relind_off[ch];
-  const double* Uc = a.upd + a.upd_off[ch];
+  const int j0 = (int)((int64_t)c * blockIdx.y / kPreChunks), j1 = (int)((int64_t)c * (blockIdx.y + 1) / kPreChunks);
+  for (int64_t i = threadIdx.x; i < (int64_t)(j1 - j0) * c; i += blockDim.x) F[(int64_t)j0 * c + i] = 0.0;
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int ib = wid; ib < uc; ib += blockDim.x / 32) {
-    double* Fc = F + (size_t)rel[ib] * c;
-    const double* Ucol = Uc + (size_t)ib * uc;
-    for (int ia = ib + lane; ia < uc; ia += 32) atomicAdd(Fc + rel[ia], Ucol[ia]);
+  for (int q = a.child_ptr[r]; q < a.child_ptr[r + 1]; ++q) {
+    const int ch = a.child_list[q];
+    const int uc = a.snc[ch] - a.sns[ch];
+    const int32_t* rel = a.relind + a.relind_off[ch];
+    const double* Uc = a.upd + a.upd_off[ch];
+    // child columns ib with rel[ib] in [j0, j1) (rel ascending: a contiguous range)
+    int lo = 0, hi = uc;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (rel[mid] < j0) lo = mid + 1;
+      else hi = mid;
+    }
+    for (int ib = lo + wid; ib < uc && rel[ib] < j1; ib += blockDim.x / 32) {
+      double* Fc = F + (size_t)rel[ib] * c;
+      const double* Ucol = Uc + (size_t)ib * uc;
+      for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
+    }
+    __syncthreads();
   }
 }
 
@@ -471,12 +462,9 @@ static CliqueArgs base_args(sdpc_ctx* h) {
 
 template <int NT, bool ALG1>
 static void launch_one(const CliqueArgs& a, const CliqueClass& k, cudaStream_t st) {
-  static bool attr_done = false;
+  static std::atomic<uint64_t> attr{0};
   auto fn = ALG1 ? alg1_kernel<NT> : mf_kernel<NT>;
-  if (!attr_done) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_done = true;
-  }
+  if (once_per_device(attr)) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   fn<<<(unsigned)k.sn.size(), NT, k.smem, st>>>(a, k.d_sn, (int)k.smem);
 }
 
@@ -550,10 +538,8 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err, in
     const auto& lev = h->a2lev[lvi];
     const int z0 = h->zero_ptr[lvi], z1 = h->zero_ptr[lvi + 1];
     if (z1 > z0) {
-      zero_fronts_kernel<<<z1 - z0, 256, 0, st>>>(h->d_zero_list + z0, h->d_ws_off, h->d.snc, a.ws);
-      const int p0 = h->pre_ptr[lvi], p1 = h->pre_ptr[lvi + 1];
-      extend_add_kernel<<<p1 - p0, 256, 0, st>>>(a, h->d_pre_child + p0, h->d_pre_parent + p0);
-      n += 2;
+      pre_extend_add_kernel<<<dim3(z1 - z0, kPreChunks), 256, 0, st>>>(a, h->d_zero_list + z0);
+      n += 1;
     }
     int used = 0;
     for (const auto& k : lev) used += k.sn.empty() ? 0 : 1;

@@ -1,16 +1,22 @@
-// (d) Dense FP64 Cholesky of the SCM, B = R R^T (lower, in place).
-// PAPER.md P:711-713 / P:735-736 / P:978-979 (type (i): LAPACK dense Cholesky with multithreaded BLAS).
-//
-// Blocked right-looking, nb = 128, with depth-1 lookahead on a second stream.  Per panel step k:
-//   diag(k)   : one CTA (512 threads) factors the 128 x 128 diagonal block in shared memory
-//               (32-column panels, one barrier per column, register-tiled panel updates) and forms
-//               L11^{-1} (blocked by 32) for the TRSM;
-//   trsm(k)   : L21 = A21 L11^{-T} as an FP64 tensor-core GEMM with the explicit inverse;
-//   ucol(k)   : trailing update of block column k+1 only (one column of 128 x 128 tiles);
-//   diag(k+1), trsm(k+1) run on the side stream while
-//   urest(k)  : the rest of the trailing update A22 -= L21 L21^T runs on the main stream.
-// GEMMs: mma.sync m8n8k4 f64 (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind), 128 x 128 CTA tiles,
-// 8 warps x (64 x 32), operands staged in shared memory by a 3-stage cp.async pipeline.
+// (d) Dense FP64 Cholesky of the SCM, B = R R^T (lower, in place): the multi-launch schedule and the tile
+// kernels.  PAPER.md P:711-713 / P:735-736 / P:978-979 (type (i): dense Cholesky with multithreaded BLAS).
+// The default one-GPU path is the persistent task-graph kernel of k_chol_dag.cu; this file serves
+//   * potrf_lower: the fallback when B cannot be staged with 16-byte copies (odd ld or unaligned B), the
+//     tile potrf of the distributed schedule (n <= 256, also returning the 128-block inverses), and
+//     sdpc_set_cholesky_schedule(h, 0);
+//   * trsm_panel / update_tiles: the panel solve and local trailing update of the distributed Cholesky
+//     (dist_chol.cu and the sdpc_trsm_panel / sdpc_update_tiles entries).
+// potrf_lower: blocked right-looking, outer block 256 (two 128 sub-panels, so the trailing updates run with
+// K = 256), depth-2 lookahead: a high-priority stream carries the critical path (update of the next block
+// column, then the next panel: diag -> trsm -> sub-panel update -> diag -> trsm) and the main stream the
+// bulk trailing update.
+//   diag : one CTA (256 threads) factors a 128 x 128 diagonal block in shared memory (32-column warp
+//          factorisations, DMMA panel rows / trailing update / off-diagonal blocks of L^{-1});
+//   trsm : L21 = A21 L11^{-T} with the explicit inverse, 64-row x 128-column tiles, 8 warps x (32 x 32),
+//          2 CTAs/SM, in place;
+//   gemm : trailing updates C -= A B^T on 128 x 64 tiles, 8 warps x (32 x 32) DMMA, 2 CTAs/SM, 16-deep
+//          k-chunks in a 4-stage cp.async pipeline, accumulators starting from C.
+// GEMMs: mma.sync m8n8k4 f64 (DMMA.8x8x4 on sm_100a; tcgen05 has no f64 kind).
 // Non-PD: the first failing column (1-based, LAPACK potrf rule) is atomicMin'ed into *err and every
 // later kernel exits at entry.
 #include <cuda_runtime.h>
@@ -562,8 +568,8 @@ static void set_gemm_attr() {  // (never for kModeTrsm: that mode launches trsm_
 constexpr int kOuter = 2 * kNB;
 
 static void set_all_attrs() {
-  static bool attr = false;
-  if (attr) return;
+  static std::atomic<uint64_t> attr{0};
+  if (!once_per_device(attr)) return;
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)diag_smem());
   cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem());
   cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem());
@@ -571,7 +577,6 @@ static void set_all_attrs() {
   set_gemm_attr<kModeUpdTri>();
   set_gemm_attr<kModeRect>();
   set_gemm_attr<kModeDist>();
-  attr = true;
 }
 
 static bool aligned16(const void* p, int64_t ld) {
@@ -591,7 +596,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
     cudaEventCreateWithFlags(&h->evB, cudaEventDisableTiming);
   }
   cudaStream_t s2 = h->st2;
-  const bool al16 = aligned16(B, ld);
+  const bool al16 = aligned16(B, ld) && aligned16(linv_ws, 2);  // the TRSM stages linv_ws with 16-byte copies
   const bool tim = h->timing;
   int launches = 0;
   double fl = 0.0;
@@ -715,7 +720,7 @@ int trsm_panel(double* A, int64_t rows, int64_t lda, const double* Lt, int64_t l
                const int32_t* d_err, cudaStream_t st) {
   set_all_attrs();
   if (rows <= 0 || kb <= 0) return 0;
-  const bool al16 = aligned16(A, lda) && aligned16(Lt, ldl);
+  const bool al16 = aligned16(A, lda) && aligned16(Lt, ldl) && aligned16(inv, 2);  // inv: 16-byte TRSM stages
   const dim3 gr((unsigned)((rows + kTile - 1) / kTile));
   int launches = 0;
   GemmArgs g{};

@@ -301,11 +301,9 @@ int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st) {
   int nl = 0;
   if (c.rows_mode) {
     const size_t smem = (size_t)2 * c.nvmax * n * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (once_per_device(attr))
       cudaFuncSetAttribute(scm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowsSmemCap);
-      attr = true;
-    }
     scm_rows_kernel<<<m, 256, smem, st>>>(n, m, h->Xh, h->Yh, c.ptr, c.ei, c.ej, c.ev, c.is_large, c.vptr, c.vlist,
                                           c.eloc, c.wdiag, c.dlist, c.ndiag, B, ldb);
   } else {

@@ -25,7 +25,7 @@
 namespace sdpc {
 
 struct SolveArgs {
-  int32_t n, nsuper, ndlev;
+  int32_t n, nsuper;
   const int32_t* super_ptr;
   const int32_t* snc;
   const int32_t* sns;
@@ -35,15 +35,12 @@ struct SolveArgs {
   const int32_t* reach_ptr;
   const int32_t* reach_sn;
   const int32_t* rhs;  // [npanels * 32] RHS vertex of each slot (elimination id), -1 = padding
-  const int32_t* dlev_ptr;
-  const int32_t* dlev_sn;
   const int32_t* border;   // backward task order: top supernodes (level order), then subtrees (preorder)
   const int32_t* sub_ptr;  // [nsub+1] offsets of the subtrees in border (starting at ntop)
   int32_t ntop, nsub;
   int32_t trunc;  // max-cut, one rank: the backward sweep stops below the panel's smallest RHS
   int32_t fac0;   // first factor of this launch (0: X-hat from L, D; 1: Y^{-1} from L_Y, D_Y)
   int32_t npanels;
-  const int32_t* sparent;
   const double* Lp[2];
   const double* D[2];
   double* out[2];
@@ -55,6 +52,7 @@ struct SolveArgs {
 };
 
 constexpr int kSolveThreads = 256;
+constexpr int kSolveSmemCap = 110 * 1024;  // opt-in of inverse_panel_kernel (2 CTAs per SM)
 
 __device__ __forceinline__ double& xrow(double* X, int row, int lane) { return X[(size_t)row * kPanelW + lane]; }
 
@@ -491,6 +489,13 @@ __global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveAr
 static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int max_ctas, const double* in,
                          double* out, bool trunc);
 
+// Dynamic shared memory of the solve kernel for nsuper supernodes (the reach bitmap grows with nsuper);
+// sdpc_create rejects problems beyond kSolveSmemCap.
+size_t solve_smem_bytes(int64_t nsuper) {
+  return sizeof(double) * (kChunk + 2 * kKc) * kVs + sizeof(uint32_t) * (((nsuper + 31) / 32) + 1);
+}
+bool solve_smem_fits(int64_t nsuper) { return solve_smem_bytes(nsuper) <= (size_t)kSolveSmemCap; }
+
 int launch_inverse_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int max_ctas) {
   return launch_panels(h, st, fac0, nfac, max_ctas, nullptr, nullptr, h->trunc_active);
 }
@@ -505,7 +510,6 @@ static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int m
   SolveArgs a{};
   a.n = h->S.n;
   a.nsuper = h->S.nsuper;
-  a.ndlev = (int32_t)h->S.dlev_ptr.size() - 1;
   a.super_ptr = h->d.super_ptr;
   a.snc = h->d.snc;
   a.sns = h->d.sns;
@@ -515,14 +519,11 @@ static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int m
   a.reach_ptr = h->d.reach_ptr;
   a.reach_sn = h->d.reach_sn;
   a.rhs = h->d.rhs;
-  a.dlev_ptr = h->d.dlev_ptr;
-  a.dlev_sn = h->d.dlev_sn;
   a.border = h->d.border;
   a.sub_ptr = h->d.sub_ptr;
   a.ntop = h->S.ntop;
   a.nsub = (int32_t)h->S.sub_ptr.size() - 1;
   a.trunc = trunc ? 1 : 0;
-  a.sparent = h->d.sparent;
   a.Lp[0] = h->Lx;
   a.Lp[1] = h->Ly;
   a.D[0] = h->Dx;
@@ -534,12 +535,10 @@ static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int m
     a.out[fac0] = out;
     a.full_sn = h->d.all_sn;
   }
-  size_t smem = sizeof(double) * (kChunk + 2 * kKc) * kVs + sizeof(uint32_t) * (((h->S.nsuper + 31) / 32) + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-    attr = true;
-  }
+  const size_t smem = solve_smem_bytes(h->S.nsuper);
+  static std::atomic<uint64_t> attr{0};
+  if (once_per_device(attr))
+    cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmemCap);
   if (h->d.npanels == 0) return 0;
   a.fac0 = fac0;
   a.npanels = h->d.npanels;

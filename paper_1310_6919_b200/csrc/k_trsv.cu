@@ -25,8 +25,9 @@ constexpr int kTb = 128;
 
 // One cooperative launch per sweep (the grid waits on itself only, inside one kernel): per 128-row
 // block, CTA 0 solves the diagonal triangle while the others wait at a grid barrier, then every CTA
-// applies the block to its share of the remaining rows (forward) / reduces its share of the dot
-// products (backward).  2 grid barriers per block instead of 2 dependent launches.
+// applies the solved block to its share of the remaining rows (both sweeps right-looking: forward
+// G[below] -= R[below, j] Y_j, backward X[above] -= R[j, above]^T X_j).  2 grid barriers per block
+// instead of 2 dependent launches.
 // Stage the lower triangle of the diagonal block [j0, j0+nb)^2 of R into Rs (upper part zero-filled)
 // with cp.async: all loads in flight at once, and issued one block ahead (R is read-only during the
 // solve), so the serial triangle solve never waits on DRAM latency.
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(256) trsv_fwd_coop(const double* __restrict__ 
 }
 
 __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ R, int64_t ldr, int64_t m, double* X,
-                                                     int64_t ldx, int nrhs, double* /*S: unused*/) {
+                                                     int64_t ldx, int nrhs) {
   extern __shared__ double trsv_sm[];
   double (*Rs)[kTb + 1] = reinterpret_cast<double (*)[kTb + 1]>(trsv_sm);
   cg::grid_group grid = cg::this_grid();
@@ -196,20 +197,26 @@ __global__ void __launch_bounds__(256) trsv_bwd_coop(const double* __restrict__ 
 int scm_solve(const double* R, int64_t ldr, int64_t m, double* G, int64_t ldg, int nrhs, double* S,
               cudaStream_t st) {
   const size_t smem = sizeof(double) * kTb * (kTb + 1);
-  static int grid = 0;
+  // cooperative grid: every CTA co-resident, sized per device (SM count and occupancy of that device)
+  static int grids[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& grid = grids[dev & 63];
   if (!grid) {
     cudaFuncSetAttribute(trsv_fwd_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(trsv_bwd_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, occ = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trsv_fwd_coop, 256, smem);
     grid = sms * std::max(1, occ);
   }
   void* fa[] = {(void*)&R, (void*)&ldr, (void*)&m, (void*)&G, (void*)&ldg, (void*)&nrhs};
-  cudaLaunchCooperativeKernel((const void*)trsv_fwd_coop, dim3(grid), dim3(256), fa, smem, st);
-  void* ba[] = {(void*)&R, (void*)&ldr, (void*)&m, (void*)&G, (void*)&ldg, (void*)&nrhs, (void*)&S};
-  cudaLaunchCooperativeKernel((const void*)trsv_bwd_coop, dim3(grid), dim3(256), ba, smem, st);
+  if (cudaLaunchCooperativeKernel((const void*)trsv_fwd_coop, dim3(grid), dim3(256), fa, smem, st) != cudaSuccess)
+    return -1;
+  void* ba[] = {(void*)&R, (void*)&ldr, (void*)&m, (void*)&G, (void*)&ldg, (void*)&nrhs};
+  (void)S;
+  if (cudaLaunchCooperativeKernel((const void*)trsv_bwd_coop, dim3(grid), dim3(256), ba, smem, st) != cudaSuccess)
+    return -1;
   return 2;
 }
 
