@@ -211,7 +211,10 @@ sdpc_status sdpc_scm_cholesky_virtual(const sdpc_handle* hs, int32_t nranks, dou
  * (SURVEY §8(f) NEXT row 2), with the factor of sdpc_scm_cholesky: (R R^T) X = G.
  *   R : DEVICE m x m column-major (ldr >= m), lower triangle = R (as left in B by the Cholesky).
  *   G : DEVICE m x nrhs column-major (ldg >= m), overwritten with X.
- * Blocked forward / backward substitution (128-row blocks); nranks == 1.
+ * Blocked forward / backward substitution (128-row blocks); nranks == 1.  The inverses of R's diagonal
+ * 128-tiles are formed first, one CTA per tile in parallel, so the serial step of each block is a
+ * 128 x 128 matrix-vector product; each sweep is one cooperative launch that reads R once (an R that is
+ * not 16-byte aligned with an even ldr solves the diagonal triangles serially instead).
  */
 sdpc_status sdpc_scm_solve(sdpc_handle h, const double* R, int64_t ldr, double* G, int64_t ldg,
                            int32_t nrhs, void* stream);

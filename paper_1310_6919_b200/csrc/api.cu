@@ -543,7 +543,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
                   h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->ws2, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
-                  h->d_err, h->d_ok, h->pair_ws, h->sce_ws, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin,
+                  h->d_err, h->d_ok, h->pair_ws, h->sce_ws, h->sce_linv, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin,
                   h->dag_ws, h->dag_linv, h->dag_koff, h->dag_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1021,19 +1021,40 @@ sdpc_status sdpc_update_tiles(sdpc_handle h, double* C, int64_t ldc, const doubl
   return SDPC_OK;
 }
 
+// The inverses of R's diagonal 128-tiles for the SCE sweeps (nullptr: unaligned R, the sweeps then solve the
+// diagonal triangles serially).
+static const double* sce_tile_inverses(sdpc_handle h, const double* R, int64_t ldr, cudaStream_t st) {
+  const int64_t m = h->S.m, T = (m + 127) / 128;
+  if (!potrf_dag_usable(R, ldr)) return nullptr;
+  if (h->sce_linv_cap < T) {
+    if (h->sce_linv) cudaFree(h->sce_linv);
+    h->sce_linv = nullptr;
+    h->sce_linv_cap = 0;
+    if (cudaMalloc(&h->sce_linv, sizeof(double) * 128 * 128 * T) != cudaSuccess) return nullptr;
+    h->sce_linv_cap = T;
+  }
+  const int l = tile_inverses(R, ldr, m, h->sce_linv, st);
+  if (l < 0) return nullptr;
+  h->launches += l;
+  return h->sce_linv;
+}
+
 sdpc_status sdpc_scm_solve(sdpc_handle h, const double* R, int64_t ldr, double* G, int64_t ldg, int32_t nrhs,
                            void* stream) {
   if (!h || !R || !G || nrhs < 1 || ldr < h->S.m || ldg < h->S.m) return SDPC_ERR_INVALID_ARG;
   if (h->nranks != 1) return SDPC_ERR_STATE;
   CK(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
-  if (h->sce_cap < nrhs) {
+  // scratch: nrhs x 128 doubles (serial-triangle sweeps) or 2 flags per 128-row block (flag sweeps)
+  const int64_t sce_need = std::max<int64_t>((int64_t)nrhs * 128, (h->S.m + 127) / 128 + 8);
+  if (h->sce_cap < sce_need) {
     if (h->sce_ws) cudaFree(h->sce_ws);
     h->sce_ws = nullptr;
-    CK(dalloc(&h->sce_ws, (size_t)nrhs * 128));
-    h->sce_cap = nrhs;
+    CK(dalloc(&h->sce_ws, (size_t)sce_need));
+    h->sce_cap = sce_need;
   }
-  const int ls = scm_solve(R, ldr, h->S.m, G, ldg, nrhs, h->sce_ws, st);
+  const double* linv = sce_tile_inverses(h, R, ldr, st);
+  const int ls = scm_solve(R, ldr, h->S.m, G, ldg, nrhs, h->sce_ws, st, linv);
   if (ls < 0) {
     h->err = "cooperative launch of the SCE solve failed";
     return SDPC_ERR_CUDA;
@@ -1061,14 +1082,16 @@ sdpc_status sdpc_search_direction(sdpc_handle h, const double* xbar_E, const dou
   if (l < 0) return SDPC_ERR_OOM;
   h->launches += l;
   const int m = h->S.m;
-  if (h->sce_cap < 1) {
+  const int64_t sce_need = std::max<int64_t>(128, (m + 127) / 128 + 8);
+  if (h->sce_cap < sce_need) {
     if (h->sce_ws) cudaFree(h->sce_ws);
     h->sce_ws = nullptr;
-    CK(dalloc(&h->sce_ws, (size_t)128));
-    h->sce_cap = 1;
+    CK(dalloc(&h->sce_ws, (size_t)sce_need));
+    h->sce_cap = sce_need;
   }
   CK(cudaMemcpyAsync(dz, g, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
-  const int ls = scm_solve(R, ldr, m, dz, m, 1, h->sce_ws, st);  // B dz = g (Eq. SCE)
+  const double* linv = sce_tile_inverses(h, R, ldr, st);
+  const int ls = scm_solve(R, ldr, m, dz, m, 1, h->sce_ws, st, linv);  // B dz = g (Eq. SCE)
   if (ls < 0) {
     h->err = "cooperative launch of the SCE solve failed";
     return SDPC_ERR_CUDA;

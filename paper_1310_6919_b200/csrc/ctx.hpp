@@ -104,7 +104,9 @@ struct sdpc_ctx {
   std::vector<int32_t> diag_ids;      // host copy of DevCons::dlist
   double* pair_ws = nullptr;          // partial sums of the diagonal-large pair reductions
   double* sce_ws = nullptr;           // scratch of sdpc_scm_solve (nrhs x 128)
-  int32_t sce_cap = 0;
+  double* sce_linv = nullptr;         // inverses of R's diagonal 128-tiles (sdpc_scm_solve)
+  int64_t sce_linv_cap = 0;
+  int64_t sce_cap = 0;
   int64_t mloc = 0, nloc = 0;      // local rows / columns of B on this rank
   sdpc::Symbolic S;
   sdpc::DevSym d;
@@ -195,6 +197,7 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
 // The same factorisation as one persistent kernel over the tile task graph (k_chol_dag.cu); needs B
 // 16-byte aligned with an even ld (potrf_dag_usable).  Returns launches (-1: workspace allocation failed).
 bool potrf_dag_usable(const double* B, int64_t ld);
+int tile_inverses(const double* R, int64_t ldr, int64_t m, double* out, cudaStream_t st);
 int potrf_dag(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st);
 // Search direction and step lengths (k_direction.cu); each returns launches or -1.
 int direction_g(sdpc_ctx* h, const double* xbar_E, const double* G_E, double bmu, double* g, cudaStream_t st);
@@ -215,6 +218,7 @@ int update_tiles(double* C, int64_t ldc, const double* P, int64_t ldp, int64_t k
                  int64_t mloc, int64_t nloc, const int32_t* d_err, cudaStream_t st, int64_t jlo, int64_t jhi);
 int launch_diag_copy(double* B, int64_t m, int64_t ld, double* out, cudaStream_t st);
 // (R R^T) X = G in place, R lower (m x m, ldr); S: nrhs x 128 doubles of scratch
-int scm_solve(const double* R, int64_t ldr, int64_t m, double* G, int64_t ldg, int nrhs, double* S, cudaStream_t st);
+int scm_solve(const double* R, int64_t ldr, int64_t m, double* G, int64_t ldg, int nrhs, double* S, cudaStream_t st,
+              const double* Linv = nullptr);
 cudaError_t fp64_peak(int device, double ms, double* dmma, double* dfma);
 }  // namespace sdpc

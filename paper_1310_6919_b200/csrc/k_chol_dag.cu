@@ -50,8 +50,14 @@ constexpr int kPotrfSmem = kPackN + NB + 32 * 36 + 32;
 constexpr int kSmem = kGemmSmem > kPotrfSmem ? kGemmSmem : kPotrfSmem;
 constexpr int kCtl = 32;         // uint32 stride between queue counters (one 128-byte line each)
 constexpr int kQ = 5;            // ready queues
-constexpr int kChainSms = 2;     // SMs whose CTAs run only the panel chain
-constexpr int kMaxSteps = 4;     // an update task applies up to this many consecutive panel steps
+#ifndef SDPC_DAG_CHAIN_SMS
+#define SDPC_DAG_CHAIN_SMS 2
+#endif
+#ifndef SDPC_DAG_MAX_STEPS
+#define SDPC_DAG_MAX_STEPS 4
+#endif
+constexpr int kChainSms = SDPC_DAG_CHAIN_SMS;  // SMs whose CTAs run only the panel chain
+constexpr int kMaxSteps = SDPC_DAG_MAX_STEPS;  // an update task applies up to this many consecutive panel steps
 
 enum : uint64_t { kPotrf = 1, kTrsm = 2, kUpd = 3 };
 
@@ -399,6 +405,32 @@ __device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double
   return -1;
 }
 
+// Inverse only (the block is already factored): lower(Ab) incl. the diagonal holds L.  Outputs as wchol32.
+__device__ __forceinline__ void wtrtri32(double* Ab, int ld, double* ldiag, double* Dq, double* col, int lane) {
+  const double dl = Ab[lane + lane * ld];
+  ldiag[lane] = dl;
+  col[lane] = 1.0 / dl;
+  __syncwarp();
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    x[i] *= col[i];
+#pragma unroll
+    for (int k = i + 1; k < 32; ++k) x[k] -= Ab[k + i * ld] * x[i];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    Dq[i * 33 + lane] = i >= lane ? x[i] : 0.0;
+    if (i >= lane) Ab[lane + i * ld] = x[i];
+  }
+}
+
+// INV_ONLY: the tile is already a Cholesky factor (R of sdpc_scm_cholesky): only its inverse is formed
+// (the SCE solve's diagonal-block inverses), also for the last tile.
+template <bool INV_ONLY = false>
 __device__ void run_potrf(const Args& a, int k, double* sm) {
   __shared__ int fail_col;
   const int k0 = k * NB, kb = a.m - k0 < NB ? a.m - k0 : NB;
@@ -434,6 +466,11 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
   for (int p = 0; p < 4; ++p) {
     const int c0 = 32 * p, ldp = pld(p);
     double* P = S + pofs(p);  // panel p: element (r, c0 + c) at P[(r - c0) + c ldp]
+    if (INV_ONLY) {
+      if (wid == 0) wtrtri32(P, ldp, ldiag + c0, Dq, Dq + 32 * 36, lane);
+      __syncthreads();
+      continue;
+    }
     if (wid == 0) {
       const int f = wchol32(P, ldp, ldiag + c0, Dq, Dq + 32 * 36, lane);
       if (lane == 0) fail_col = f;
@@ -494,13 +531,13 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
   }
   // L to B: warp w writes columns w, w + 8, ..., lanes over rows (coalesced)
 #pragma unroll 1
-  for (int j = wid; j < kb; j += kThreads / 32) {
+  for (int j = INV_ONLY ? kb : wid; j < kb; j += kThreads / 32) {
     const int p = j >> 5;
     const double* col = S + pofs(p) + (j & 31) * pld(p) - 32 * p;  // element i at col[i], i >= 32 p
     for (int i = j + lane; i < kb; i += 32) __stcg(Bd + i + (int64_t)j * a.ld, i == j ? ldiag[i] : col[i]);
   }
   if (pt && tid == 0) pt[6] = gtimer();
-  if (k == a.T - 1) return;  // no panel below the last tile: its inverse is not needed
+  if (!INV_ONLY && k == a.T - 1) return;  // no panel below the last tile: its inverse is not needed
   // L^{-1} in shared memory, in place by block rows I = 1..3 and columns J < I (ascending):
   //   T = sum_{K=J}^{I-1} L[I,K] Linv[K,J]  (L[I,K] for K >= J is still L: only columns < J of row I are
   //   overwritten yet);  Linv[I,J] = -Dinv_I T  replaces L[I,J] (panel J, rows 32 I ..).
@@ -673,7 +710,32 @@ __global__ void __launch_bounds__(kThreads, 2) chol_dag_kernel(Args a) {
   }
 }
 
+// The inverses of the T diagonal 128-tiles of a Cholesky factor, one CTA per tile (all in parallel).
+__global__ void __launch_bounds__(kThreads, 2) tile_inverse_kernel(Args a) {
+  extern __shared__ double sm[];
+  run_potrf<true>(a, blockIdx.x, sm);
+}
+
 }  // namespace dag
+
+// out[k] (128 x 128 column-major, zero above the diagonal, identity-padded for a ragged last tile) <- the
+// inverse of the k-th 128 x 128 diagonal block of the lower factor R (m x m, ldr).  Needs 16-byte staging
+// (potrf_dag_usable); returns launches or -1.
+int tile_inverses(const double* R, int64_t ldr, int64_t m, double* out, cudaStream_t st) {
+  using namespace dag;
+  if (!potrf_dag_usable(R, ldr) || m <= 0) return -1;
+  static std::atomic<uint64_t> attr{0};
+  if (once_per_device(attr))
+    cudaFuncSetAttribute(tile_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem * (int)sizeof(double));
+  Args a{};
+  a.B = const_cast<double*>(R);
+  a.ld = ldr;
+  a.m = (int)m;
+  a.T = (int)((m + NB - 1) / NB);
+  a.Linv = out;
+  tile_inverse_kernel<<<a.T, kThreads, kSmem * sizeof(double), st>>>(a);
+  return 1;
+}
 
 // Workspace sizes for T tiles.
 struct DagSizes {

@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
 // q) zeroes the front's columns of chunk q and adds, child by child in a fixed order, the children's
 // update columns that land there (warp per column, distinct columns within a child, a barrier between
 // children).  Columns are owned by one CTA: no atomics, deterministic summation order.
-constexpr int kPreChunks = 8;
+constexpr int kPreChunks = 64;  // column ranges per front: parallelism of the fixed-order child loop
 __global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
   const int r = list[blockIdx.x];
   const int c = a.snc[r];
@@ -430,8 +430,8 @@ __global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const
       else hi = mid;
     }
     for (int ib = lo + wid; ib < uc && rel[ib] < j1; ib += blockDim.x / 32) {
-      double* Fc = F + (size_t)rel[ib] * c;
-      const double* Ucol = Uc + (size_t)ib * uc;
+      double* __restrict__ Fc = F + (size_t)rel[ib] * c;
+      const double* __restrict__ Ucol = Uc + (size_t)ib * uc;
       for (int ia = ib + lane; ia < uc; ia += 32) Fc[rel[ia]] += Ucol[ia];
     }
     __syncthreads();

@@ -389,7 +389,7 @@ def test_fused_iteration_not_pd_phases():
     assert e.value.info == 1
 
 
-@pytest.mark.parametrize("m,nrhs", [(1, 1), (129, 2), (1000, 1), (1311, 3)])
+@pytest.mark.parametrize("m,nrhs", [(1, 1), (129, 2), (1000, 1), (1311, 3), (2048, 1), (3000, 4)])
 def test_sce_solve_with_scm_factor(m, nrhs):
     """NEXT row 2 (SCE): sdpc_scm_solve with the factor of sdpc_scm_cholesky against the
     oracle's LAPACK solve, ragged sizes and several right-hand sides."""
@@ -399,11 +399,14 @@ def test_sce_solve_with_scm_factor(m, nrhs):
     rng = np.random.default_rng(m + nrhs)
     G = rng.standard_normal((m, m + 4))
     Bh = G @ G.T / (m + 4) + 0.5 * np.eye(m)
-    Bt = torch.from_numpy(np.tril(Bh).T.copy()).to(dev)           # column-major lower
-    assert h.scm_cholesky(Bt, m) == 0
+    # even ld: the sweeps use the diagonal-tile inverses (16-byte staging); odd m: the serial triangles
+    ld = m + (m & 1) if m % 3 else m
+    Bt = torch.zeros((m, ld), dtype=torch.float64, device=dev)
+    Bt[:, :m] = torch.from_numpy(np.tril(Bh).T.copy()).to(dev)    # column-major lower
+    assert h.scm_cholesky(Bt, ld) == 0
     Rhs = rng.standard_normal((m, nrhs))
     Gt = torch.from_numpy(Rhs.T.copy()).to(dev)                    # column-major m x nrhs
-    h.scm_solve(Bt, Gt, m, m, nrhs)
+    h.scm_solve(Bt, Gt, ld, m, nrhs)
     X = Gt.cpu().numpy().T
     Xo = CH.sce_solve(Bh, Rhs)
     assert rel(X, Xo) < 1e-10
