@@ -60,6 +60,10 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return y;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   int sz = valid ? 16 : 0;

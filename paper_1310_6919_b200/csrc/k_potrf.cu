@@ -381,7 +381,15 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, const int tile, dou
     cp_async_commit();
   }
 
-  // accumulators: C (updates; lower part only where the tile meets the diagonal) or zero (TRSM)
+  // accumulators: C for tiles off the diagonal (textbook update order); zero for TRSM and for tiles
+  // that meet the diagonal, whose O(1) entries get C added once in the epilogue (one rounding per
+  // launch instead of one per DMMA: see k_chol_dag.cu), C prefetched into L2 meanwhile
+  const bool cadd = UPD && mask;
+  if (cadd)
+    for (int q = tid; q < (nbv < kBN ? nbv : kBN) * (kTile / 16); q += kGemmThreads) {
+      const int c = q / (kTile / 16), r = (q % (kTile / 16)) * 16;
+      if (r < na) prefetch_l2(Cb + r + (size_t)c * g.ldc);
+    }
   double acc[kWA][4][2];
 #pragma unroll
   for (int a = 0; a < kWA; ++a) {
@@ -391,7 +399,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, const int tile, dou
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = wn * 32 + b * 8 + 2 * t4 + e;
-        acc[a][b][e] = (UPD && i < na && j < nbv && (!mask || j + doff <= i)) ? Cb[i + (size_t)j * g.ldc] : 0.0;
+        acc[a][b][e] = (UPD && !mask && i < na && j < nbv) ? Cb[i + (size_t)j * g.ldc] : 0.0;
       }
   }
 
@@ -430,7 +438,10 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, const int tile, dou
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = wn * 32 + b * 8 + 2 * t4 + e;
-        if (j < nbv && (!mask || j + doff <= i)) Cb[i + (size_t)j * g.ldc] = acc[a][b][e];
+        if (j < nbv && (!mask || j + doff <= i)) {
+          double* cp = Cb + i + (size_t)j * g.ldc;
+          *cp = cadd ? *cp + acc[a][b][e] : acc[a][b][e];
+        }
       }
   }
 }
