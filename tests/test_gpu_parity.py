@@ -466,9 +466,8 @@ def gen_config_md0():
 @pytest.mark.parametrize("cfg", [1, 3])
 def test_cholesky_full_size_elementwise(cfg):
     """(d) at full size, element-wise against LAPACK potrf of the GPU's own B:
-    ||R_gpu - R_lapack||_F / ||R_lapack||_F <= 1e-10, and the backward error ||B - R R^T|| / ||B|| no worse
-    than twice LAPACK's own on the same B (SURVEY's 1e-14 sits below the rounding of the check itself,
-    numpy's R R^T over 10^4-term sums, at m = 10,000)."""
+    ||R_gpu - R_lapack||_F / ||R_lapack||_F <= 1e-10, and the backward error ||B - R R^T||_F / ||B||_F <= 1e-14
+    (LAPACK's own is ~2e-16 here, the GPU factor's ~5e-16)."""
     from instances import gen_config
     inst = gen_config(cfg)
     g = run_gpu(inst, ld=inst.m + (inst.m & 1), chol=False)
@@ -478,4 +477,4 @@ def test_cholesky_full_size_elementwise(cfg):
     R = np.tril(g["Bt"][:, :m].T.cpu().numpy())
     Ro = CH.potrf_lower(B)
     assert rel(R, Ro) < TOL_R
-    assert CH.backward_error(B, R) <= max(1e-14, 2.0 * CH.backward_error(B, Ro))
+    assert CH.backward_error(B, R) <= 1e-14
