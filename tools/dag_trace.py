@@ -101,3 +101,21 @@ for b in range(10):
 names = ["load", "p0", "p1", "p2", "p3", "Lstore", "Linv"]
 d = np.diff(pst[:-1], axis=1) / 1e3
 print("POTRF phases (us, mean over k < T-1): " + "  ".join(f"{nm} {v:.1f}" for nm, v in zip(names, d.mean(axis=0))))
+
+# the panel chain step by step in the tail: POTRF(k) end -> TRSM(k+1, k, *) -> UPD(k+1, k+1, k, *) -> POTRF(k+1)
+ii = (tr[:, 0] >> 16) & 0xffff
+jj = tr[:, 0] & 0xffff
+rows = []
+for kk in range(max(0, T - 31), T - 1):
+    pe_k = t1[(typ == 1) & (k == kk)]
+    ts = np.where((typ == 2) & (k == kk) & (ii == kk + 1))[0]
+    us = np.where((typ == 3) & (ii == kk + 1) & (jj == kk + 1) & (k + nsteps - 1 == kk))[0]
+    pn = t0[(typ == 1) & (k == kk + 1)]
+    if len(pe_k) and len(ts) and len(us) and len(pn):
+        rows.append([t0[ts].min() - pe_k[0], (t1[ts] - t0[ts]).max(), t0[us].min() - t1[ts].max(),
+                     (t1[us] - t0[us]).max(), pn[0] - t1[us].max(),
+                     (t1[(typ == 1) & (k == kk + 1)] - pn)[0]])
+if rows:
+    r = np.array(rows) / 1e3
+    nm = ["POTRF->TRSM gap", "TRSM", "TRSM->UPD gap", "UPD(diag)", "UPD->POTRF gap", "POTRF"]
+    print("tail chain (us, mean over the last %d steps): " % len(r) + "  ".join(f"{a} {b:.1f}" for a, b in zip(nm, r.mean(0))))
