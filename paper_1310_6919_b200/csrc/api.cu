@@ -204,7 +204,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     for (int32_t q = S.hlev_ptr[lv]; q < S.hlev_ptr[lv + 1]; ++q) {
       const int32_t r = S.hlev_sn[q];
       const int32_t nch = S.child_ptr[r + 1] - S.child_ptr[r];
-      if (ws_off[r] >= 0 && nch > 2) {
+      if (ws_off[r] >= 0) {  // every global front: the pre-pass assembles it (big-front path)
         pre[r] = 1;
         zero_list.push_back(r);
         for (int32_t cq = S.child_ptr[r]; cq < S.child_ptr[r + 1]; ++cq) {
@@ -218,8 +218,25 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   }
   h->pre_ptr = pre_ptr;
   h->zero_ptr = zero_ptr;
+  // global-workspace fronts take the big-front path (front_panel_kernel + front_schur_kernel), the rest
+  // the per-front class kernels
+  std::vector<int32_t> big_list;
+  h->big_ptr.assign(nh + 1, 0);
+  h->big_tiles.assign(nh, 0);
   for (int lv = 0; lv < nh; ++lv) {
-    std::vector<int32_t> mem(S.hlev_sn.begin() + S.hlev_ptr[lv], S.hlev_sn.begin() + S.hlev_ptr[lv + 1]);
+    std::vector<int32_t> mem;
+    for (int32_t q = S.hlev_ptr[lv]; q < S.hlev_ptr[lv + 1]; ++q) {
+      const int32_t r = S.hlev_sn[q];
+      if (ws_off[r] >= 0) {
+        big_list.push_back(r);
+        const int64_t u = S.snc[r] - S.sns[r], t64 = (u + 63) / 64;
+        h->big_tiles[lv] = std::max<int32_t>(h->big_tiles[lv], (int32_t)(t64 * (t64 + 1) / 2));
+        h->big_smem = std::max(h->big_smem, std::min(kPanelCap, pb[r]));
+      } else {
+        mem.push_back(r);
+      }
+    }
+    h->big_ptr[lv + 1] = (int32_t)big_list.size();
     std::stable_sort(mem.begin(), mem.end(), [&](int32_t x, int32_t y) { return S.snc[x] > S.snc[y]; });
     if (build_classes(h->a2lev[lv], mem, b2, ws_off, pb) != cudaSuccess) return fail(SDPC_ERR_OOM);
   }
@@ -466,6 +483,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   UP(h->d_pre_child, pre_child);
   UP(h->d_pre_parent, pre_parent);
   UP(h->d_zero_list, zero_list);
+  UP(h->d_big_list, big_list);
   DevCons& cs = h->cons;
   cs.maxcut = maxcut;
   cs.m = m;
@@ -539,7 +557,7 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   d.umap, d.relind_off, d.relind, d.upd_off, d.child_ptr, d.child_list, d.hlev_sn,
                   d.dlev_ptr, d.dlev_sn, d.preorder, d.border, d.sub_ptr, d.perm, d.iperm, d.reach_ptr, d.reach_sn, d.rhs, d.slot_of, d.all_sn, d.sym_ptr, d.sym_col, d.sym_pos, d.ecs_ptr, d.ecs_k,
                   d.ecs_val, d.cons_epos, h->Uh, h->dir_ws, h->d_step_off, h->step_ws, h->d_amin, h->ytmp, h->d_ws_off, h->d_pre, h->d_pre_child,
-                  h->d_pre_parent, h->d_zero_list,
+                  h->d_pre_parent, h->d_zero_list, h->d_big_list,
                   h->cons.ptr, h->cons.ei, h->cons.ej, h->cons.ev, h->cons.is_large, h->cons.large,
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
                   h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->ws2, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,

@@ -122,6 +122,10 @@ struct sdpc_ctx {
   int32_t* d_pre_parent = nullptr;
   int32_t* d_zero_list = nullptr;
   std::vector<int32_t> pre_ptr, zero_ptr;
+  // (a2) big fronts (global workspace) per etree height: list offsets, max Schur tiles, panel smem
+  std::vector<int32_t> big_ptr, big_tiles;
+  int32_t* d_big_list = nullptr;
+  size_t big_smem = 0;
   double* Lx = nullptr;          // X factor panels
   double* Dx = nullptr;
   double* Ly = nullptr;          // Y factor panels

@@ -276,6 +276,26 @@ __device__ __forceinline__ void tile_gemm(const double* A, int64_t lda, const do
         acc[x][y][e] = (UPD && !mask && i < na && jc < nbv) ? __ldcg(C + i + (int64_t)jc * ldc) : 0.0;
       }
   }
+  // a diagonal tile adds each 128-deep step's sum to C separately (the same rounding whatever the number
+  // of steps a task applies: bitwise reproducible under the run-dependent absorption); each thread
+  // owns its C entries, so no barrier is needed
+  auto flush_c = [&]() {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int i = wm * 32 + x * 8 + g8;
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int jc = wn * 32 + y * 8 + 2 * t4 + e;
+          if (i < na && jc < nbv && jc + doff <= i) {
+            double* cp = C + i + (int64_t)jc * ldc;
+            __stcg(cp, __ldcg(cp) + acc[x][y][e]);
+          }
+          acc[x][y][e] = 0.0;
+        }
+    }
+  };
 #pragma unroll 1
   for (int kc = 0; kc < nk; ++kc) {
     cp_async_wait<kStages - 2>();
@@ -300,6 +320,7 @@ __device__ __forceinline__ void tile_gemm(const double* A, int64_t lda, const do
 #pragma unroll
         for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
     }
+    if (cadd && (kc + 1) % (NB / kBK) == 0 && kc + 1 < nk) flush_c();
   }
   cp_async_wait<0>();
   if (!UPD) __syncthreads();  // in place: every warp has staged its A rows before any is overwritten

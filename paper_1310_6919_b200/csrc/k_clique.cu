@@ -124,8 +124,10 @@ __device__ __forceinline__ void warp_chol_inv32(double* A, int ld, int j0, int j
 // CTA-cooperative blocked Cholesky of the leading `ncols` columns of the symmetric c x c matrix A
 // (lower triangle, column-major, leading dimension ld = c), with the trailing block updated.
 // Returns the failing column index, or -1.
+// lim: the trailing update is restricted to columns < lim (the big-front path factors only the pivot
+// panel here and forms the Schur complement in front_schur_kernel; lim = c otherwise).
 template <int NT, bool GLOBAL>
-__device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
+__device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s, int lim = 0x7fffffff) {
   const int tid = threadIdx.x, wid = tid >> 5;
   const int ld = c;
   for (int j0 = 0; j0 < ncols; j0 += 32) {
@@ -159,7 +161,10 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
       // trailing update of rows/cols >= r0: A[i,j] -= sum_k P[i,k] P[j,k] on the FP64 tensor cores,
       // one 8 x 8 lower tile per warp task (m8n8k4 DMMA, K = jw), C read-modify-written in place
       const int lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
-      const int nb8 = (nr + 7) >> 3, ntile = nb8 * (nb8 + 1) / 2;
+      const int nb8 = (nr + 7) >> 3;
+      const int jl = min(lim, c);                             // columns < jl are updated
+      const int nbj = min(nb8, (jl - r0 + 7) >> 3);            // tile columns kept
+      const int ntri = nbj * (nbj + 1) / 2, ntile = ntri + (nb8 - nbj) * nbj;
       constexpr int kB = 4;  // tiles per warp batch: their C loads are in flight together
       for (int t0 = wid * kB; t0 < ntile; t0 += (NT / 32) * kB) {
         double c0[kB], c1[kB];
@@ -167,16 +172,22 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
           const int t = t0 + b;
-          int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-          while (ti * (ti + 1) / 2 > t) --ti;
-          while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-          const int tj = t - ti * (ti + 1) / 2;
+          int ti, tj;
+          if (t < ntri) {  // triangle of the kept tile columns, then the rectangle below it
+            ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while (ti * (ti + 1) / 2 > t) --ti;
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            tj = t - ti * (ti + 1) / 2;
+          } else {
+            ti = nbj + (t - ntri) / nbj;
+            tj = (t - ntri) % nbj;
+          }
           ii[b] = t < ntile ? r0 + ti * 8 : c;  // c: empty tile
           jj[b] = r0 + tj * 8;
           const int i = ii[b] + g8, j = jj[b] + 2 * t4;
           const bool iv = i < c;
-          c0[b] = (iv && j < c && j <= i) ? A[i + (size_t)j * ld] : 0.0;
-          c1[b] = (iv && j + 1 < c && j + 1 <= i) ? A[i + (size_t)(j + 1) * ld] : 0.0;
+          c0[b] = (iv && j < jl && j <= i) ? A[i + (size_t)j * ld] : 0.0;
+          c1[b] = (iv && j + 1 < jl && j + 1 <= i) ? A[i + (size_t)(j + 1) * ld] : 0.0;
         }
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
@@ -193,8 +204,8 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s) {
         for (int b = 0; b < kB; ++b) {
           const int i = ii[b] + g8, j = jj[b] + 2 * t4;
           const bool iv = i < c;
-          if (iv && j < c && j <= i) A[i + (size_t)j * ld] = c0[b];
-          if (iv && j + 1 < c && j + 1 <= i) A[i + (size_t)(j + 1) * ld] = c1[b];
+          if (iv && j < jl && j <= i) A[i + (size_t)j * ld] = c0[b];
+          if (iv && j + 1 < jl && j + 1 <= i) A[i + (size_t)(j + 1) * ld] = c1[b];
         }
       }
     }
@@ -438,6 +449,104 @@ __global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const
   }
 }
 
+// (a2) big fronts (global workspace), one front over many CTAs: the pre-pass assembles the front
+// (zero + children's extend-add, column ranges per CTA); front_panel_kernel (one CTA per front) adds
+// Y's pivot columns and factors the |S_r| pivot columns only (L~ = L D^{1/2} in place, L_Y, D_Y out);
+// front_schur_kernel (64 x 64 tiles of the update matrix over CTAs) forms U_r = F_UU - L~_U L~_U^T on the
+// tensor cores straight into the update-matrix storage.  Same arithmetic as mf_kernel,
+// with the Schur complement no longer streamed through a single SM.
+template <int NT>
+__global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int32_t* __restrict__ list, int pbytes) {
+  extern __shared__ double smem[];
+  __shared__ double inv[32 * kLdInv], l11[32 * kLdInv];
+  __shared__ int flag;
+  const int r = list[blockIdx.x];
+  const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
+  double* F = a.ws + a.ws_off[r];
+  const int tid = threadIdx.x;
+  const int64_t* __restrict__ colptr = a.colptr;
+  for (int64_t idx = tid; idx < (int64_t)c * s; idx += NT) {
+    const int i = (int)(idx % c), j = (int)(idx / c);
+    if (i >= j) F[idx] += a.vals[colptr[f + j] + (i - j)];
+  }
+  __syncthreads();
+  double* panel = ((size_t)c * 32 * sizeof(double) <= (size_t)pbytes) ? smem : F + (size_t)c * c + (size_t)c * s;
+  Scratch sc{inv, l11, panel, &flag};
+  const int fail = cta_chol_partial<NT, true>(F, c, s, sc, s);
+  if (fail >= 0) {
+    if (tid == 0) report_error(a.err, f + fail);
+    return;
+  }
+  double* Lp = a.Lp + a.panel_off[r];
+  for (int64_t idx = tid; idx < (int64_t)c * s; idx += NT) {
+    const int ar = (int)(idx % c), t = (int)(idx / c);
+    const double dg = F[t + (size_t)t * c];
+    Lp[idx] = ar > t ? F[idx] / dg : (ar == t ? 1.0 : 0.0);
+  }
+  for (int t = tid; t < s; t += NT) {
+    const double dg = F[t + (size_t)t * c];
+    a.D[f + t] = dg * dg;
+  }
+}
+
+constexpr int kSchurT = 64, kSchurK = 32, kSchurLd = kSchurT + 4;
+__global__ void __launch_bounds__(256) front_schur_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
+  __shared__ __align__(16) double As[kSchurK * kSchurLd], Bs[kSchurK * kSchurLd];
+  const int r = list[blockIdx.y];
+  const int s = a.sns[r], c = a.snc[r], u = c - s;
+  const int nt = (u + kSchurT - 1) / kSchurT;
+  const int t = blockIdx.x;
+  if (t >= nt * (nt + 1) / 2 || *(const volatile int32_t*)a.err != kNoError) return;
+  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while (ti * (ti + 1) / 2 > t) --ti;
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  const int tj = t - ti * (ti + 1) / 2;
+  const double* F = a.ws + a.ws_off[r];
+  double* Ur = a.upd + a.upd_off[r];
+  const int a0 = ti * kSchurT, b0 = tj * kSchurT;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int wm = wid & 1, wn = wid >> 1;  // warp tile: rows 32 wm .. +32, columns 16 wn .. +16
+  double acc[4][2][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  for (int k0 = 0; k0 < s; k0 += kSchurK) {
+    __syncthreads();
+    for (int q = tid; q < kSchurK * kSchurT; q += 256) {
+      const int kk = q / kSchurT, i = q % kSchurT;
+      const bool kv = k0 + kk < s;
+      As[kk * kSchurLd + i] = (kv && a0 + i < u) ? F[(s + a0 + i) + (size_t)(k0 + kk) * c] : 0.0;
+      Bs[kk * kSchurLd + i] = (kv && b0 + i < u) ? F[(s + b0 + i) + (size_t)(k0 + kk) * c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k4 = 0; k4 < kSchurK; k4 += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) af[x] = As[(k4 + t4) * kSchurLd + 32 * wm + 8 * x + g8];
+#pragma unroll
+      for (int y = 0; y < 2; ++y) bf[y] = Bs[(k4 + t4) * kSchurLd + 16 * wn + 8 * y + g8];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int ia = a0 + 32 * wm + 8 * x + g8;
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ib = b0 + 16 * wn + 8 * y + 2 * t4 + e;
+        if (ia < u && ib <= ia) Ur[ia + (size_t)ib * u] = F[(s + ia) + (size_t)(s + ib) * c] - acc[x][y][e];
+      }
+  }
+}
+
 static CliqueArgs base_args(sdpc_ctx* h) {
   CliqueArgs a{};
   a.super_ptr = h->d.super_ptr;
@@ -543,12 +652,22 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err, in
     }
     int used = 0;
     for (const auto& k : lev) used += k.sn.empty() ? 0 : 1;
-    if (used <= 1) {
+    const int b0 = h->big_ptr[lvi], nbig = h->big_ptr[lvi + 1] - b0;
+    if (nbig == 0 && used <= 1) {
       n += launch_classes<false>(a, lev, st);
       continue;
     }
     cudaEvent_t fk = set ? h->fork_ev2 : h->fork_ev;
-    cudaEventRecord(fk, st);
+    if (used > 0) cudaEventRecord(fk, st);
+    if (nbig > 0) {  // big fronts on the level's own stream, concurrent with the class kernels
+      static std::atomic<uint64_t> attr{0};
+      if (once_per_device(attr))
+        cudaFuncSetAttribute(front_panel_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      front_panel_kernel<256><<<nbig, 256, h->big_smem, st>>>(a, h->d_big_list + b0, (int)h->big_smem);
+      if (h->big_tiles[lvi] > 0)
+        front_schur_kernel<<<dim3(h->big_tiles[lvi], nbig), 256, 0, st>>>(a, h->d_big_list + b0);
+      n += 1 + (h->big_tiles[lvi] > 0);
+    }
     for (int q = 0; q < (int)lev.size() && q < 4; ++q) {
       if (lev[q].sn.empty()) continue;
       cudaStreamWaitEvent(h->sides[set][q], fk, 0);
