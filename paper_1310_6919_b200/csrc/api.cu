@@ -510,7 +510,34 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
     h->err = cudaGetErrorString(e);                   \
     return fail(SDPC_ERR_OOM);                        \
   }
-  AL(h->ws, (size_t)ws_total);
+  // (a1): the global-workspace cliques (a1cls[3]) take the big-clique pipeline with its own workspace
+  // (A with an even leading dimension for the task kernels' 16-byte staging, then W); h->ws is unused
+  {
+    const auto& big = h->a1cls[3].sn;
+    h->nbig1 = (int32_t)big.size();
+    std::vector<int64_t> boff(big.size());
+    std::vector<int32_t> bdim(big.size());
+    int64_t tot = 0;
+    h->big1_c.resize(big.size());
+    for (size_t b = 0; b < big.size(); ++b) {
+      const int64_t c = S.snc[big[b]], sc = S.sns[big[b]];
+      boff[b] = tot;
+      bdim[b] = (int32_t)c;
+      h->big1_c[b] = (int32_t)c;
+      tot += c * (c + (c & 1)) + c * sc;
+      tot += tot & 1;
+    }
+    if (!big.empty()) {
+      if ((e = upload(&h->big1_off, boff)) != cudaSuccess || (e = upload(&h->big1_dim, bdim)) != cudaSuccess) {
+        h->err = cudaGetErrorString(e);
+        return fail(SDPC_ERR_OOM);
+      }
+      AL(h->big1_ws, (size_t)tot);
+      AL(h->big1_linv, big.size() * 128 * 128);
+      AL(h->big1_err, big.size());
+    }
+  }
+  AL(h->ws, 1);
   AL(h->ws2, (size_t)ws_total);
   AL(h->Lx, (size_t)S.panel_total);
   AL(h->Ly, (size_t)S.panel_total);
@@ -562,7 +589,8 @@ sdpc_status sdpc_destroy(sdpc_handle h) {
                   h->cons.vrow, h->cons.aval, h->cons.col_cons, h->cons.vptr, h->cons.vlist, h->cons.eloc,
                   h->cons.diag_large, h->cons.wdiag, h->cons.dlist, h->ws, h->ws2, h->Lx, h->Ly, h->Dx, h->Dy, h->upd,
                   h->d_err, h->d_ok, h->pair_ws, h->sce_ws, h->sce_linv, h->potrf_ws, h->Xh, h->Yh, h->Bown, h->xin, h->yin,
-                  h->dag_ws, h->dag_linv, h->dag_koff, h->dag_trace};
+                  h->dag_ws, h->dag_linv, h->dag_koff, h->dag_trace, h->big1_off, h->big1_dim, h->big1_err,
+                  h->big1_ws, h->big1_linv};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->pinned_in) cudaFreeHost(h->pinned_in);

@@ -124,6 +124,14 @@ struct sdpc_ctx {
   std::vector<int32_t> pre_ptr, zero_ptr;
   // (a2) big fronts (global workspace) per etree height: list offsets, max Schur tiles, panel smem
   std::vector<int32_t> big_ptr, big_tiles;
+  // (a1) big cliques (a1cls[3], decreasing c): workspace offsets / dims / error slots, L^{-1} buffers
+  int32_t nbig1 = 0;
+  std::vector<int32_t> big1_c;
+  int64_t* big1_off = nullptr;
+  int32_t* big1_dim = nullptr;
+  int32_t* big1_err = nullptr;
+  double* big1_ws = nullptr;
+  double* big1_linv = nullptr;
   int32_t* d_big_list = nullptr;
   size_t big_smem = 0;
   double* Lx = nullptr;          // X factor panels
@@ -203,6 +211,19 @@ int potrf_lower(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, c
 bool potrf_dag_usable(const double* B, int64_t ld);
 int tile_inverses(const double* R, int64_t ldr, int64_t m, double* out, cudaStream_t st);
 int potrf_dag(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cudaStream_t st);
+// Batched right-looking Cholesky (k_chol_dag.cu), step q over the first nact matrices (sorted by
+// decreasing dim; maxdim = dim of the first).  Matrix b: base + off[b], ld = dim + (dim & 1), 16-byte
+// aligned.  err_slot[b] (kNoError-initialised) records its failure, err_id[b] is reported into *err.
+struct BatchDesc {
+  double* base;
+  const int64_t* off;
+  const int32_t* dim;
+  int32_t* err_slot;
+  const int32_t* err_id;
+  int32_t* err;
+  double* linv;  // [nbatch][128 * 128]
+};
+int batched_chol_step(const BatchDesc& d, int q, int nact, int maxdim, cudaStream_t st);
 // Search direction and step lengths (k_direction.cu); each returns launches or -1.
 int direction_g(sdpc_ctx* h, const double* xbar_E, const double* G_E, double bmu, double* g, cudaStream_t st);
 int direction_dY_dX(sdpc_ctx* h, const double* xbar_E, const double* G_E, double bmu, const double* dz, double* dY_E,

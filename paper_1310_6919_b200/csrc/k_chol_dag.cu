@@ -750,7 +750,78 @@ __global__ void __launch_bounds__(kThreads, 2) tile_inverse_kernel(Args a) {
   run_potrf<true>(a, blockIdx.x, sm);
 }
 
+// ------------------------------------------------------------------ batched dense Cholesky steps
+// Step q of the blocked right-looking Cholesky of many independent matrices at once (the big cliques
+// of Algorithm 1, Step 2-2): matrix b is dim[b] x dim[b] at base + off[b] (column-major, ld = dim + (dim
+// & 1), 16-byte aligned); the matrices are sorted by decreasing dim, so the ones still active at step q
+// are a prefix (gridDim.y).  Three launches per step, each a batch of the task-graph kernel's own
+// tasks: POTRF(q) of every matrix (L_qq^{-1} to its own 128 x 128 buffer), TRSM(i, q, *) and
+// UPD(i, j, q, *).  A failing matrix reports err_id[b] (its clique) into *err and its later steps are
+// skipped.
+__device__ __forceinline__ bool batch_args(const BatchDesc& d, int b, int q, Args& a) {
+  const int m = d.dim[b];
+  if (*(const volatile int32_t*)(d.err_slot + b) != kNoError || 128 * q >= m) return false;
+  a = Args{};
+  a.B = d.base + d.off[b];
+  a.ld = m + (m & 1);
+  a.m = m;
+  a.T = (m + NB - 1) / NB;
+  a.Linv = d.linv + (int64_t)b * NB * NB - (int64_t)q * NB * NB;  // run_* index Linv + q NB NB
+  a.err = d.err_slot + b;
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) batch_potrf_kernel(BatchDesc d, int q) {
+  extern __shared__ double sm[];
+  Args a;
+  const int b = blockIdx.x;
+  if (!batch_args(d, b, q, a)) return;
+  run_potrf(a, q, sm);
+  __syncthreads();
+  if (threadIdx.x == 0 && *(volatile int32_t*)a.err != kNoError) report_error(d.err, d.err_id[b]);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) batch_trsm_kernel(BatchDesc d, int q) {
+  extern __shared__ double sm[];
+  Args a;
+  if (!batch_args(d, blockIdx.y, q, a)) return;
+  const int i = q + 1 + (int)(blockIdx.x >> 1);
+  if (i >= a.T) return;
+  run_trsm(a, q, i, blockIdx.x & 1, sm);
+}
+
+__global__ void __launch_bounds__(kThreads, 2) batch_upd_kernel(BatchDesc d, int q) {
+  extern __shared__ double sm[];
+  Args a;
+  if (!batch_args(d, blockIdx.y, q, a)) return;
+  const int t = blockIdx.x >> 1;  // lower-triangle tile (i, j), q < j <= i < T, row-major
+  int r = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while (r * (r + 1) / 2 > t) --r;
+  while ((r + 1) * (r + 2) / 2 <= t) ++r;
+  const int i = q + 1 + r, j = q + 1 + (t - r * (r + 1) / 2);
+  if (i >= a.T) return;
+  run_upd(a, q, 1, i, j, blockIdx.x & 1, sm);
+}
+
 }  // namespace dag
+
+int batched_chol_step(const BatchDesc& d, int q, int nact, int maxdim, cudaStream_t st) {
+  using namespace dag;
+  static std::atomic<uint64_t> attr{0};
+  if (once_per_device(attr)) {
+    cudaFuncSetAttribute(batch_potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem * (int)sizeof(double));
+    cudaFuncSetAttribute(batch_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem * (int)sizeof(double));
+    cudaFuncSetAttribute(batch_upd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem * (int)sizeof(double));
+  }
+  if (nact <= 0) return 0;
+  const int T = (maxdim + NB - 1) / NB, below = T - q - 1;
+  const size_t smem = kSmem * sizeof(double);
+  batch_potrf_kernel<<<nact, kThreads, smem, st>>>(d, q);
+  if (below <= 0) return 1;
+  batch_trsm_kernel<<<dim3(2 * below, nact), kThreads, smem, st>>>(d, q);
+  batch_upd_kernel<<<dim3(below * (below + 1), nact), kThreads, smem, st>>>(d, q);
+  return 3;
+}
 
 // out[k] (128 x 128 column-major, zero above the diagonal, identity-padded for a ragged last tile) <- the
 // inverse of the k-th 128 x 128 diagonal block of the lower factor R (m x m, ldr).  Needs 16-byte staging

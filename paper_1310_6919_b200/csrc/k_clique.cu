@@ -217,7 +217,8 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s, i
 // W (c x s, ld c) = M^{-T} [0; I_s]: blocked back substitution from the last 32-row block up.
 // M lower (A, ld c).  Column t of W is nonzero only in rows <= u + t.
 template <int NT>
-__device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, const Scratch& sc) {
+__device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, const Scratch& sc, int lda = 0) {
+  if (lda == 0) lda = c;  // leading dimension of M (W: ld c)
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int u = c - s;
   for (int idx = tid; idx < c * s; idx += NT) {
@@ -240,7 +241,7 @@ __device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, 
       for (int task = wid; task < nq8 * nt8; task += NT / 32) {
         const int qb = (task % nq8) * 8, tb = t0 + (task / nq8) * 8;
         const int qa = qb + g8, ta = tb + g8;
-        const double* Ap = A + lo + (size_t)(jb + qa) * c;
+        const double* Ap = A + lo + (size_t)(jb + qa) * lda;
         const double* Bp = W + lo + (size_t)ta * c;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll 4
@@ -262,8 +263,8 @@ __device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, 
       for (int i = 0; i < 32; ++i) {
         double sacc = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
-        for (int k = 0; k < i; ++k) sacc -= ((i < jw && k < jw) ? A[(jb + i) + (size_t)(jb + k) * c] : 0.0) * x[k];
-        const double dii = (i < jw) ? A[(jb + i) + (size_t)(jb + i) * c] : 1.0;
+        for (int k = 0; k < i; ++k) sacc -= ((i < jw && k < jw) ? A[(jb + i) + (size_t)(jb + k) * lda] : 0.0) * x[k];
+        const double dii = (i < jw) ? A[(jb + i) + (size_t)(jb + i) * lda] : 1.0;
         x[i] = sacc / dii;
       }
 #pragma unroll
@@ -547,6 +548,62 @@ __global__ void __launch_bounds__(256) front_schur_kernel(CliqueArgs a, const in
   }
 }
 
+// (a1) big cliques (global workspace), Algorithm 1 over many CTAs: Step 2-1 (gather of the reversed
+// clique matrix) by CTAs owning column ranges; Step 2-2 (Cholesky M M^T) by the batched task kernels
+// of k_chol_dag.cu (POTRF / TRSM / UPD steps over every big clique at once); Step 2-3 (last |S_r| rows
+// of M^{-1}) and Step 3 by one CTA per clique.  The same arithmetic as alg1_kernel.
+// Workspace of big clique b: A (c x ld, ld = c + (c & 1), 16-byte aligned) then W (c x s, ld c).
+constexpr int kBigGatherChunks = 32;
+__global__ void __launch_bounds__(256) big_gather_kernel(CliqueArgs a, const int32_t* __restrict__ list,
+                                                         const int64_t* __restrict__ off, double* base) {
+  const int r = list[blockIdx.y];
+  const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s, ld = c + (c & 1);
+  double* A = base + off[blockIdx.y];
+  const int j0 = (int)((int64_t)c * blockIdx.x / kBigGatherChunks), j1 = (int)((int64_t)c * (blockIdx.x + 1) / kBigGatherChunks);
+  const int64_t uo = a.umap_off[r];
+  for (int jp = j0; jp < j1; ++jp)
+    for (int ip = jp + threadIdx.x; ip < c; ip += blockDim.x) {
+      const int ai = c - 1 - ip, bi = c - 1 - jp;  // ai <= bi: X[bi, ai] (lower)
+      double v;
+      if (ai < s) {
+        v = a.vals[a.colptr[f + ai] + (bi - ai)];
+      } else {
+        const int64_t ap = ai - s, bp = bi - s;
+        v = a.vals[a.umap[uo + ap * u - ap * (ap - 1) / 2 + (bp - ap)]];
+      }
+      A[ip + (size_t)jp * ld] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) big_backsub_kernel(CliqueArgs a, const int32_t* __restrict__ list,
+                                                          const int64_t* __restrict__ off, double* base,
+                                                          const int32_t* __restrict__ err_slot) {
+  __shared__ double inv[32 * kLdInv], l11[32 * kLdInv];
+  __shared__ int flag;
+  const int b = blockIdx.x;
+  if (err_slot[b] != kNoError) return;
+  const int r = list[b];
+  const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], ld = c + (c & 1);
+  const double* A = base + off[b];
+  double* W = base + off[b] + (size_t)c * ld;
+  Scratch sc{inv, l11, nullptr, &flag};
+  cta_backsub_last_rows<256>(A, W, c, s, sc, ld);
+  const int tid = threadIdx.x;
+  double* Lp = a.Lp + a.panel_off[r];
+  for (int idx = tid; idx < c * s; idx += 256) {
+    const int ar = idx % c, t = idx / c;
+    const double dg = W[(c - 1 - t) + (size_t)(s - 1 - t) * c];
+    double v;
+    if (ar > t) v = W[(c - 1 - ar) + (size_t)(s - 1 - t) * c] / dg;
+    else v = (ar == t) ? 1.0 : 0.0;
+    Lp[idx] = v;
+  }
+  for (int t = tid; t < s; t += 256) {
+    const double dg = W[(c - 1 - t) + (size_t)(s - 1 - t) * c];
+    a.D[f + t] = dg * dg;
+  }
+}
+
 static CliqueArgs base_args(sdpc_ctx* h) {
   CliqueArgs a{};
   a.super_ptr = h->d.super_ptr;
@@ -623,6 +680,22 @@ int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
   int n = 0;
   for (int q = 0; q < (int)h->a1cls.size() && q < 4; ++q) {
     cudaStreamWaitEvent(h->side[q], h->fork_ev, 0);
+    if (q == 3 && h->nbig1 > 0) {  // global-workspace cliques: the multi-CTA big-clique pipeline
+      cudaStream_t s3 = h->side[q];
+      cudaMemsetAsync(h->big1_err, 0x7f, (size_t)h->nbig1 * sizeof(int32_t), s3);
+      big_gather_kernel<<<dim3(kBigGatherChunks, h->nbig1), 256, 0, s3>>>(a, h->a1cls[3].d_sn, h->big1_off, h->big1_ws);
+      BatchDesc d{h->big1_ws, h->big1_off, h->big1_dim, h->big1_err, h->a1cls[3].d_sn, h->d_err, h->big1_linv};
+      n += 2;
+      for (int st = 0; 128 * st < h->big1_c[0]; ++st) {
+        int nact = 0;
+        while (nact < h->nbig1 && h->big1_c[nact] > 128 * st) ++nact;
+        n += batched_chol_step(d, st, nact, h->big1_c[0], s3);
+      }
+      big_backsub_kernel<<<h->nbig1, 256, 0, s3>>>(a, h->a1cls[3].d_sn, h->big1_off, h->big1_ws, h->big1_err);
+      cudaEventRecord(h->side_ev[q], s3);
+      cudaStreamWaitEvent(st, h->side_ev[q], 0);
+      continue;
+    }
     std::vector<CliqueClass> one(1, h->a1cls[q]);
     n += launch_classes<true>(a, one, h->side[q]);
     one[0].d_sn = nullptr;  // not owned here
