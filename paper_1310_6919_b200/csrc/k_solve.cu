@@ -101,6 +101,66 @@ __device__ __forceinline__ void bwd_supernode(const double* __restrict__ Lr, int
   }
 }
 
+// backward for one supernode with |S_r| > 8, one warp, FP64 tensor cores: per 16-column chunk, the
+// gathered-row product acc(j, n) = sum_q L[q][t0 + j] x[row(q)][n] as m8n8k4 DMMA tiles (2 row tiles x
+// 4 RHS slices, K = the rows after the chunk), no per-FMA shuffles; the accumulators go through a
+// per-warp shared-memory square (Wm, 16 x 33) to the lane = RHS layout of the chunk triangle.
+__device__ __forceinline__ void bwd_supernode_mma(const double* __restrict__ Lr, int c, int s, int f,
+                                                  const int32_t* __restrict__ U, double* X, int lane, bool onpath,
+                                                  double* Wm) {
+  constexpr int kCh = 16;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  for (int t1 = s; t1 > 0; t1 -= kCh) {
+    const int t0 = t1 > kCh ? t1 - kCh : 0;
+    const int w = t1 - t0;
+    const double* Lc = Lr + (size_t)t0 * c;  // Lc[i + j*c] = L[i, t0+j]
+    double d[2][4][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+    const int K = c - t1;
+#pragma unroll 2
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int q = t1 + k0 + t4;
+      const bool kv = k0 + t4 < K;
+      const int row = kv ? (q < s ? f + q : U[q - s]) : 0;
+      double av[2], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) av[mt] = (kv && 8 * mt + g8 < w) ? Lc[q + (size_t)(8 * mt + g8) * c] : 0.0;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = kv ? X[(size_t)row * kPanelW + 8 * nt + g8] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(d[mt][nt][0], d[mt][nt][1], av[mt], bv[nt]);
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        Wm[(8 * mt + g8) * 33 + 8 * nt + 2 * t4] = d[mt][nt][0];
+        Wm[(8 * mt + g8) * 33 + 8 * nt + 2 * t4 + 1] = d[mt][nt][1];
+      }
+    __syncwarp();
+    double acc[kCh];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j)
+      acc[j] = j < w ? (onpath ? xrow(X, f + t0 + j, lane) : 0.0) - Wm[j * 33 + lane] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int j = kCh - 1; j >= 0; --j) {
+      if (j < w) {
+        const double xj = acc[j];
+        xrow(X, f + t0 + j, lane) = xj;
+#pragma unroll
+        for (int jj = 0; jj < j; ++jj) acc[jj] -= Lc[(t0 + j) + (size_t)jj * c] * xj;
+      }
+    }
+    __syncwarp();  // this chunk's rows are read (as gathered rows) by the next chunk
+  }
+}
+
 // ---- big supernodes (|S_r| >= kBigS): whole CTA, FP64 tensor cores (m8n8k4 DMMA) -------------
 // The rectangular parts of both sweeps are small GEMMs whose operands come straight from L2:
 // A = a block of the supernode panel L_r, B = 8-RHS slices of gathered rows of the panel X, so
@@ -345,14 +405,26 @@ __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, 
     for (int j = 0; j < kCh; ++j)
       if (j < s) zslot[j * kPanelW + lane] = zt[j];
   }
+  // rows U in groups of 4 per warp: independent row / L loads in flight (a tall thin supernode, e.g. the
+  // top separator chain of a 3D torus with |U| ~ 1400, is otherwise a chain of dependent L2 round trips)
   const int u = c - s;
-  for (int qq = wid; qq < u; qq += nw) {
-    const int row = U[qq];
-    double acc = xrow(X, row, lane);
+  for (int q0 = 4 * wid; q0 < u; q0 += 4 * nw) {
+    int row[4];
+    double acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      row[e] = q0 + e < u ? U[q0 + e] : -1;
+      acc[e] = row[e] >= 0 ? xrow(X, row[e], lane) : 0.0;
+    }
 #pragma unroll
     for (int j = 0; j < kCh; ++j)
-      if (j < s) acc -= Lr[s + qq + (size_t)j * c] * zt[j];
-    xrow(X, row, lane) = acc;
+      if (j < s)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (q0 + e < u) acc[e] -= Lr[s + q0 + e + (size_t)j * c] * zt[j];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (row[e] >= 0) xrow(X, row[e], lane) = acc[e];
   }
 }
 
@@ -470,7 +542,7 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
       else if (s <= 2) bwd_supernode<2>(Lr, c, s, f, U, X, lane, onpath);
       else if (s <= 4) bwd_supernode<4>(Lr, c, s, f, U, X, lane, onpath);
       else if (s <= 8) bwd_supernode<8>(Lr, c, s, f, U, X, lane, onpath);
-      else bwd_supernode<16>(Lr, c, s, f, U, X, lane, onpath);
+      else bwd_supernode_mma(Lr, c, s, f, U, X, lane, onpath, Vs + wid * (16 * 33));
     }
   }
 }
