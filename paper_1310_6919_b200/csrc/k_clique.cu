@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(NT) mf_kernel(CliqueArgs a, const int32_t* __r
 // q) zeroes the front's columns of chunk q and adds, child by child in a fixed order, the children's
 // update columns that land there (warp per column, distinct columns within a child, a barrier between
 // children).  Columns are owned by one CTA: no atomics, deterministic summation order.
-constexpr int kPreChunks = 64;  // column ranges per front: parallelism of the fixed-order child loop
+constexpr int kPreChunks = 128;  // column ranges per front: parallelism of the fixed-order child loop
 __global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
   const int r = list[blockIdx.x];
   const int c = a.snc[r];
@@ -466,9 +466,10 @@ __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int
   double* F = a.ws + a.ws_off[r];
   const int tid = threadIdx.x;
   const int64_t* __restrict__ colptr = a.colptr;
-  for (int64_t idx = tid; idx < (int64_t)c * s; idx += NT) {
-    const int i = (int)(idx % c), j = (int)(idx / c);
-    if (i >= j) F[idx] += a.vals[colptr[f + j] + (i - j)];
+  for (int j = 0; j < s; ++j) {  // (2D loops: no 64-bit division per element)
+    const double* yc = a.vals + colptr[f + j] - j;
+    double* Fc = F + (size_t)j * c;
+    for (int i = j + tid; i < c; i += NT) Fc[i] += yc[i];
   }
   __syncthreads();
   double* panel = ((size_t)c * 32 * sizeof(double) <= (size_t)pbytes) ? smem : F + (size_t)c * c + (size_t)c * s;
@@ -479,14 +480,12 @@ __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int
     return;
   }
   double* Lp = a.Lp + a.panel_off[r];
-  for (int64_t idx = tid; idx < (int64_t)c * s; idx += NT) {
-    const int ar = (int)(idx % c), t = (int)(idx / c);
-    const double dg = F[t + (size_t)t * c];
-    Lp[idx] = ar > t ? F[idx] / dg : (ar == t ? 1.0 : 0.0);
-  }
-  for (int t = tid; t < s; t += NT) {
-    const double dg = F[t + (size_t)t * c];
-    a.D[f + t] = dg * dg;
+  for (int t = 0; t < s; ++t) {
+    const double dg = F[t + (size_t)t * c], rdg = 1.0 / dg;
+    const double* Fc = F + (size_t)t * c;
+    double* Lc = Lp + (size_t)t * c;
+    for (int ar = tid; ar < c; ar += NT) Lc[ar] = ar > t ? Fc[ar] * rdg : (ar == t ? 1.0 : 0.0);
+    if (tid == 0) a.D[f + t] = dg * dg;
   }
 }
 
