@@ -296,6 +296,47 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
     const int t0 = ch * kChunk, w = min(kChunk, s - t0), t1 = t0 + w;
     const int ntt = (w + 7) >> 3, ntask = ntt * 4;
     const int K = c - t1;  // gathered rows: S after the chunk, then U
+    if (w <= 16) {
+      // thin chunk (e.g. the 8-13-column separator supernodes of a 3D torus with |U| ~ 1,400-2,900): the
+      // K rows are split over the warps instead of the output tiles (each warp: both row tiles x four
+      // RHS slices, operands straight from L2, no staging barriers), partial sums reduced through Bs
+      const int Kw = ((K + 4 * nw - 1) / (4 * nw)) * 4, kb = wid * Kw, ke = min(K, kb + Kw);
+      double d[2][4][2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) d[mt][nt][0] = d[mt][nt][1] = 0.0;
+#pragma unroll 2
+      for (int k0 = kb; k0 < ke; k0 += 4) {
+        const int q = t1 + k0 + t4;
+        const bool kv = k0 + t4 < ke;
+        const int row = kv ? op_row(q, f, s, U) : 0;
+        double av[2], bv[4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) av[mt] = (kv && 8 * mt + g8 < w) ? Lr[q + (size_t)(t0 + 8 * mt + g8) * c] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) bv[nt] = kv ? X[(size_t)row * kPanelW + 8 * nt + g8] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(d[mt][nt][0], d[mt][nt][1], av[mt], bv[nt]);
+      }
+      double* red = Bs + wid * (16 * 33);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          red[(8 * mt + g8) * 33 + 8 * nt + 2 * t4] = d[mt][nt][0];
+          red[(8 * mt + g8) * 33 + 8 * nt + 2 * t4 + 1] = d[mt][nt][1];
+        }
+      __syncthreads();
+      for (int idx = tid; idx < w * kPanelW; idx += nw * 32) {
+        const int r = idx >> 5, n = idx & 31;
+        double sum = 0.0;
+        for (int v = 0; v < nw; ++v) sum += Bs[v * (16 * 33) + r * 33 + n];
+        Vs[r * kVs + n] = (onpath ? X[(size_t)(f + t0 + r) * kPanelW + n] : 0.0) - sum;
+      }
+    } else {
     double acc[kMaxTasks][2];
 #pragma unroll
     for (int q = 0; q < kMaxTasks; ++q) acc[q][0] = acc[q][1] = 0.0;
@@ -349,6 +390,7 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
         }
       }
     }
+    }  // (w > 16)
     __syncthreads();
     // chunk triangle L_cc^T, 16-row diagonal blocks from the bottom up
     const int nb = (w + 15) / 16;
