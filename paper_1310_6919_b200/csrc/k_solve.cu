@@ -433,7 +433,7 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
 template <int kCh>
 __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, int s, int f,
                                           const int32_t* __restrict__ U, double* X, double* zslot, int lane,
-                                          int wid, int nw) {
+                                          int wid, int nw, double* zw) {
   double zt[kCh];
 #pragma unroll
   for (int j = 0; j < kCh; ++j) zt[j] = j < s ? xrow(X, f + j, lane) : 0.0;
@@ -447,9 +447,57 @@ __device__ __forceinline__ void fwd_small(const double* __restrict__ Lr, int c, 
     for (int j = 0; j < kCh; ++j)
       if (j < s) zslot[j * kPanelW + lane] = zt[j];
   }
-  // rows U in groups of 4 per warp: independent row / L loads in flight (a tall thin supernode, e.g. the
-  // top separator chain of a 3D torus with |U| ~ 1400, is otherwise a chain of dependent L2 round trips)
   const int u = c - s;
+  constexpr int KQ = kCh >= 8 ? kCh / 4 : 1;
+  if constexpr (kCh >= 8) if (u >= 128) {
+    // tall supernode (e.g. the top separator chain of a 3D torus, |U| ~ 1,400-2,900): x[U] -= L_US z[S] as
+    // m8n8k4 DMMA tiles (8 rows of U x 8 RHS), z[S] as B fragments through a per-warp shared square, two
+    // row tiles per warp in flight
+    const int g8 = lane >> 2, t4 = lane & 3;
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) zw[j * 33 + lane] = zt[j];
+    __syncwarp();
+    double bv[KQ][4];
+#pragma unroll
+    for (int kq = 0; kq < KQ; ++kq)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[kq][nt] = zw[(4 * kq + t4) * 33 + 8 * nt + g8];
+    const int ntile = (u + 7) >> 3;
+    for (int t = wid; t < ntile; t += 2 * nw) {
+      int row[2];
+      double av[2][KQ], cc[2][4][2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int q = 8 * (t + e * nw) + g8;
+        const bool qv = t + e * nw < ntile && q < u;
+        row[e] = qv ? U[q] : -1;
+#pragma unroll
+        for (int kq = 0; kq < KQ; ++kq)
+          av[e][kq] = (qv && 4 * kq + t4 < s) ? -Lr[s + q + (size_t)(4 * kq + t4) * c] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          cc[e][nt][0] = qv ? X[(size_t)row[e] * kPanelW + 8 * nt + 2 * t4] : 0.0;
+          cc[e][nt][1] = qv ? X[(size_t)row[e] * kPanelW + 8 * nt + 2 * t4 + 1] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int kq = 0; kq < KQ; ++kq)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma_8x8x4(cc[e][nt][0], cc[e][nt][1], av[e][kq], bv[kq][nt]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (row[e] >= 0)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            X[(size_t)row[e] * kPanelW + 8 * nt + 2 * t4] = cc[e][nt][0];
+            X[(size_t)row[e] * kPanelW + 8 * nt + 2 * t4 + 1] = cc[e][nt][1];
+          }
+    }
+    return;
+  }
+  // rows U in groups of 4 per warp: independent row / L loads in flight
   for (int q0 = 4 * wid; q0 < u; q0 += 4 * nw) {
     int row[4];
     double acc[4];
@@ -530,11 +578,11 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
     } else {
       const int32_t* U = rowind + a.colptr[f] + s;
       double* zs = zslots + slot * 16 * kPanelW;
-      if (s <= 1) fwd_small<1>(Lr, c, s, f, U, X, zs, lane, wid, NW);
-      else if (s <= 2) fwd_small<2>(Lr, c, s, f, U, X, zs, lane, wid, NW);
-      else if (s <= 4) fwd_small<4>(Lr, c, s, f, U, X, zs, lane, wid, NW);
-      else if (s <= 8) fwd_small<8>(Lr, c, s, f, U, X, zs, lane, wid, NW);
-      else fwd_small<16>(Lr, c, s, f, U, X, zs, lane, wid, NW);
+      if (s <= 1) fwd_small<1>(Lr, c, s, f, U, X, zs, lane, wid, NW, Vs + wid * (16 * 33));
+      else if (s <= 2) fwd_small<2>(Lr, c, s, f, U, X, zs, lane, wid, NW, Vs + wid * (16 * 33));
+      else if (s <= 4) fwd_small<4>(Lr, c, s, f, U, X, zs, lane, wid, NW, Vs + wid * (16 * 33));
+      else if (s <= 8) fwd_small<8>(Lr, c, s, f, U, X, zs, lane, wid, NW, Vs + wid * (16 * 33));
+      else fwd_small<16>(Lr, c, s, f, U, X, zs, lane, wid, NW, Vs + wid * (16 * 33));
       pend_f = f;
       pend_s = s;
       pend_slot = slot;
