@@ -223,6 +223,8 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
   std::vector<int32_t> big_list;
   h->big_ptr.assign(nh + 1, 0);
   h->big_tiles.assign(nh, 0);
+  h->big_thin.assign(nh, 0);
+  h->big_wide.assign(nh, 0);
   for (int lv = 0; lv < nh; ++lv) {
     std::vector<int32_t> mem;
     for (int32_t q = S.hlev_ptr[lv]; q < S.hlev_ptr[lv + 1]; ++q) {
@@ -231,6 +233,7 @@ sdpc_status sdpc_create(sdpc_handle* out, int32_t n, int32_t m, const int64_t* a
         big_list.push_back(r);
         const int64_t u = S.snc[r] - S.sns[r], t64 = (u + 63) / 64;
         h->big_tiles[lv] = std::max<int32_t>(h->big_tiles[lv], (int32_t)(t64 * (t64 + 1) / 2));
+        (S.sns[r] <= 32 ? h->big_thin : h->big_wide)[lv] = 1;  // (kThinS in k_clique.cu)
         h->big_smem = std::max(h->big_smem, std::min(kPanelCap, pb[r]));
       } else {
         mem.push_back(r);

@@ -124,6 +124,7 @@ struct sdpc_ctx {
   std::vector<int32_t> pre_ptr, zero_ptr;
   // (a2) big fronts (global workspace) per etree height: list offsets, max Schur tiles, panel smem
   std::vector<int32_t> big_ptr, big_tiles;
+  std::vector<uint8_t> big_thin, big_wide;  // level has big fronts with |S| <= 32 / > 32
   // (a1) big cliques (a1cls[3], decreasing c): workspace offsets / dims / error slots, L^{-1} buffers
   int32_t nbig1 = 0;
   std::vector<int32_t> big1_c;

@@ -456,6 +456,8 @@ __global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const
 // front_schur_kernel (64 x 64 tiles of the update matrix over CTAs) forms U_r = F_UU - L~_U L~_U^T on the
 // tensor cores straight into the update-matrix storage.  Same arithmetic as mf_kernel,
 // with the Schur complement no longer streamed through a single SM.
+constexpr int kThinS = 32;  // fronts with at most this many pivots: front_thin_kernel
+
 template <int NT>
 __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int32_t* __restrict__ list, int pbytes) {
   extern __shared__ double smem[];
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int
   __shared__ int flag;
   const int r = list[blockIdx.x];
   const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r];
+  if (s <= kThinS) return;  // front_thin_kernel
   double* F = a.ws + a.ws_off[r];
   const int tid = threadIdx.x;
   const int64_t* __restrict__ colptr = a.colptr;
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(256) front_schur_kernel(CliqueArgs a, const in
   const int s = a.sns[r], c = a.snc[r], u = c - s;
   const int nt = (u + kSchurT - 1) / kSchurT;
   const int t = blockIdx.x;
-  if (t >= nt * (nt + 1) / 2 || *(const volatile int32_t*)a.err != kNoError) return;
+  if (s <= kThinS || t >= nt * (nt + 1) / 2 || *(const volatile int32_t*)a.err != kNoError) return;
   int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while (ti * (ti + 1) / 2 > t) --ti;
   while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
@@ -603,6 +606,111 @@ __global__ void __launch_bounds__(256) big_backsub_kernel(CliqueArgs a, const in
   }
 }
 
+// Thin big fronts (|S_r| <= 32, e.g. the separator chain of a 3D torus: s ~ 8-13, |C_r| ~ 1,400-2,900):
+// pivot panel and update matrix in ONE launch.  Every CTA (a 64 x 64 tile of U_r) factors the s x s
+// pivot block F_SS + Y_SS itself (one warp, registers: a few microseconds), forms the L~ rows of its
+// tile rows and columns, L~_U = F_US L~_SS^{-T}, and applies U_r = F_UU - L~_U L~_U^T on the tensor cores;
+// diagonal tiles also write their L rows (unit form) and CTA 0 the pivot block and D_Y.  Same arithmetic
+// as front_panel_kernel + front_schur_kernel.
+__global__ void __launch_bounds__(256) front_thin_kernel(CliqueArgs a, const int32_t* __restrict__ list) {
+  __shared__ __align__(16) double As[kSchurK * kSchurLd], Bs[kSchurK * kSchurLd];
+  __shared__ double inv[32 * kLdInv], dg[32];
+  __shared__ int flag;
+  double* a11 = Bs;  // the pivot block and the warp's staging square live in Bs / As until the L~ rows
+  const int r = list[blockIdx.y];
+  const int f = a.super_ptr[r], s = a.sns[r], c = a.snc[r], u = c - s;
+  if (s > kThinS) return;
+  const int nt = (u + kSchurT - 1) / kSchurT;
+  const int t = blockIdx.x;
+  if (t >= max(1, nt * (nt + 1) / 2)) return;
+  const double* F = a.ws + a.ws_off[r];
+  const double* __restrict__ Y = a.vals;
+  const int64_t* __restrict__ colptr = a.colptr;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // pivot block F_SS + Y_SS (lower), factored and inverted by warp 0
+  for (int idx = tid; idx < 32 * 32; idx += 256) {
+    const int i = idx & 31, j = idx >> 5;
+    a11[i + j * kLdInv] = (i < s && j < s && i >= j) ? F[i + (size_t)j * c] + Y[colptr[f + j] + (i - j)] : 0.0;
+  }
+  __syncthreads();
+  Scratch sc{inv, As, nullptr, &flag};
+  if (wid == 0) warp_chol_inv32(a11, kLdInv, 0, s, sc);
+  __syncthreads();
+  if (flag >= 0) {
+    if (t == 0 && tid == 0) report_error(a.err, f + flag);
+    return;
+  }
+  double* Lp = a.Lp + a.panel_off[r];
+  if (t == 0) {  // pivot block rows of the unit-form panel, D_Y
+    for (int idx = tid; idx < s * s; idx += 256) {
+      const int ar = idx % s, k = idx / s;
+      Lp[ar + (size_t)k * c] = ar > k ? a11[ar + k * kLdInv] / a11[k + k * kLdInv] : (ar == k ? 1.0 : 0.0);
+    }
+    for (int k = tid; k < s; k += 256) a.D[f + k] = a11[k + k * kLdInv] * a11[k + k * kLdInv];
+  }
+  if (tid < 32) dg[tid] = tid < s ? a11[tid + tid * kLdInv] : 1.0;
+  __syncthreads();  // a11 (Bs) and the staging square (As) are overwritten below
+  int ti = 0, tj = 0;
+  if (u > 0) {
+    ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (ti * (ti + 1) / 2 > t) --ti;
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    tj = t - ti * (ti + 1) / 2;
+  }
+  const int a0 = ti * kSchurT, b0 = tj * kSchurT;
+  // L~ rows: L~[s + a][k] = sum_{q <= k} (F + Y)[s + a][q] Linv[k][q]   (inv(k, q) at inv[k + q * kLdInv])
+  for (int idx = tid; idx < 2 * kSchurT * kSchurK; idx += 256) {
+    const int which = idx / (kSchurT * kSchurK), rem = idx % (kSchurT * kSchurK);
+    const int i = rem % kSchurT, k = rem / kSchurT;
+    const int aa = (which ? b0 : a0) + i;
+    double v = 0.0;
+    if (aa < u && k < s) {
+      const int row = s + aa;
+      for (int q = 0; q <= k; ++q) v += (F[row + (size_t)q * c] + Y[colptr[f + q] + (row - q)]) * inv[k + q * kLdInv];
+    }
+    (which ? Bs : As)[k * kSchurLd + i] = v;
+  }
+  __syncthreads();
+  if (u == 0) return;
+  if (ti == tj)
+    for (int idx = tid; idx < kSchurT * s; idx += 256) {
+      const int i = idx % kSchurT, k = idx / kSchurT;
+      if (a0 + i < u) Lp[(s + a0 + i) + (size_t)k * c] = As[k * kSchurLd + i] / dg[k];
+    }
+  double* Ur = a.upd + a.upd_off[r];
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int wm = wid & 1, wn = wid >> 1;
+  double acc[4][2][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+#pragma unroll 2
+  for (int k4 = 0; k4 < kSchurK; k4 += 4) {
+    if (k4 >= s) break;
+    double af[4], bf[2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) af[x] = As[(k4 + t4) * kSchurLd + 32 * wm + 8 * x + g8];
+#pragma unroll
+    for (int y = 0; y < 2; ++y) bf[y] = Bs[(k4 + t4) * kSchurLd + 16 * wn + 8 * y + g8];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int ia = a0 + 32 * wm + 8 * x + g8;
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int ib = b0 + 16 * wn + 8 * y + 2 * t4 + e;
+        if (ia < u && ib <= ia) Ur[ia + (size_t)ib * u] = F[(s + ia) + (size_t)(s + ib) * c] - acc[x][y][e];
+      }
+  }
+}
+
 static CliqueArgs base_args(sdpc_ctx* h) {
   CliqueArgs a{};
   a.super_ptr = h->d.super_ptr;
@@ -685,10 +793,10 @@ int launch_alg1(sdpc_ctx* h, const double* xbar, cudaStream_t st) {
       big_gather_kernel<<<dim3(kBigGatherChunks, h->nbig1), 256, 0, s3>>>(a, h->a1cls[3].d_sn, h->big1_off, h->big1_ws);
       BatchDesc d{h->big1_ws, h->big1_off, h->big1_dim, h->big1_err, h->a1cls[3].d_sn, h->d_err, h->big1_linv};
       n += 2;
-      for (int st = 0; 128 * st < h->big1_c[0]; ++st) {
+      for (int stp = 0; 128 * stp < h->big1_c[0]; ++stp) {
         int nact = 0;
-        while (nact < h->nbig1 && h->big1_c[nact] > 128 * st) ++nact;
-        n += batched_chol_step(d, st, nact, h->big1_c[0], s3);
+        while (nact < h->nbig1 && h->big1_c[nact] > 128 * stp) ++nact;
+        n += batched_chol_step(d, stp, nact, h->big1_c[0], s3);
       }
       big_backsub_kernel<<<h->nbig1, 256, 0, s3>>>(a, h->a1cls[3].d_sn, h->big1_off, h->big1_ws, h->big1_err);
       cudaEventRecord(h->side_ev[q], s3);
@@ -735,10 +843,16 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err, in
       static std::atomic<uint64_t> attr{0};
       if (once_per_device(attr))
         cudaFuncSetAttribute(front_panel_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      front_panel_kernel<256><<<nbig, 256, h->big_smem, st>>>(a, h->d_big_list + b0, (int)h->big_smem);
-      if (h->big_tiles[lvi] > 0)
-        front_schur_kernel<<<dim3(h->big_tiles[lvi], nbig), 256, 0, st>>>(a, h->d_big_list + b0);
-      n += 1 + (h->big_tiles[lvi] > 0);
+      if (h->big_wide[lvi]) {
+        front_panel_kernel<256><<<nbig, 256, h->big_smem, st>>>(a, h->d_big_list + b0, (int)h->big_smem);
+        if (h->big_tiles[lvi] > 0)
+          front_schur_kernel<<<dim3(h->big_tiles[lvi], nbig), 256, 0, st>>>(a, h->d_big_list + b0);
+        n += 1 + (h->big_tiles[lvi] > 0);
+      }
+      if (h->big_thin[lvi]) {
+        front_thin_kernel<<<dim3(std::max(1, h->big_tiles[lvi]), nbig), 256, 0, st>>>(a, h->d_big_list + b0);
+        n += 1;
+      }
     }
     for (int q = 0; q < (int)lev.size() && q < 4; ++q) {
       if (lev[q].sn.empty()) continue;
