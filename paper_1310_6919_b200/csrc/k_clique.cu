@@ -165,7 +165,7 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s, i
       const int jl = min(lim, c);                             // columns < jl are updated
       const int nbj = min(nb8, (jl - r0 + 7) >> 3);            // tile columns kept
       const int ntri = nbj * (nbj + 1) / 2, ntile = ntri + (nb8 - nbj) * nbj;
-      constexpr int kB = 4;  // tiles per warp batch: their C loads are in flight together
+      constexpr int kB = 8;  // tiles per warp batch: their C loads are in flight together
       for (int t0 = wid * kB; t0 < ntile; t0 += (NT / 32) * kB) {
         double c0[kB], c1[kB];
         int ii[kB], jj[kB];
