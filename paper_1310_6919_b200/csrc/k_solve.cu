@@ -195,8 +195,9 @@ __device__ __forceinline__ void tile_gemm_gather(double& c0, double& c1, const d
 }
 
 // forward, big supernode r: z[S] = L_SS^{-1} z[S] (chunks ascending), then z[U] -= L_US z[S]
+constexpr int kLs = 129;  // stride of the staged 16-column strips of L (chunk triangles)
 __device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, const int32_t* __restrict__ U,
-                        double* X, double* Vs, int tid, int lane, int wid, int nw) {
+                        double* X, double* Vs, double* Ls, int tid, int lane, int wid, int nw) {
   const int g8 = lane >> 2, t4 = lane & 3;
   for (int t0 = 0; t0 < s; t0 += kChunk) {
     const int w = min(kChunk, s - t0);
@@ -223,9 +224,16 @@ __device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, cons
       }
     }
     __syncthreads();
-    // chunk triangle, 16-row diagonal blocks
+    // chunk triangle, 16-row diagonal blocks; the block's 16 columns of L (rows b0 .. w of the chunk) are
+    // staged in shared memory first (Ls[j * kLs + t] = L[t0 + t][t0 + b0 + j]), so the per-row updates read
+    // L with broadcast LDS instead of dependent L2 round trips
     for (int b0 = 0; b0 < w; b0 += 16) {
       const int bw = min(16, w - b0);
+      for (int idx = tid; idx < 16 * (w - b0); idx += nw * 32) {
+        const int j = idx / (w - b0), t = b0 + idx % (w - b0);
+        Ls[j * kLs + t] = j < bw ? Lr[(t0 + t) + (size_t)(t0 + b0 + j) * c] : 0.0;
+      }
+      __syncthreads();
       if (wid == 0) {
         double acc[16];
 #pragma unroll
@@ -234,7 +242,7 @@ __device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, cons
         for (int j = 0; j < 16; ++j) {
 #pragma unroll
           for (int jj = j + 1; jj < 16; ++jj)
-            if (jj < bw) acc[jj] -= Lr[(t0 + b0 + jj) + (size_t)(t0 + b0 + j) * c] * acc[j];
+            if (jj < bw) acc[jj] -= Ls[j * kLs + b0 + jj] * acc[j];
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j)
@@ -245,7 +253,7 @@ __device__ void big_fwd(const double* __restrict__ Lr, int c, int s, int f, cons
         double v = Vs[t * kVs + lane];
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (j < bw) v -= Lr[(t0 + t) + (size_t)(t0 + b0 + j) * c] * Vs[(b0 + j) * kVs + lane];
+          if (j < bw) v -= Ls[j * kLs + t] * Vs[(b0 + j) * kVs + lane];
         Vs[t * kVs + lane] = v;
       }
       __syncthreads();
@@ -396,6 +404,12 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
     const int nb = (w + 15) / 16;
     for (int bb = nb - 1; bb >= 0; --bb) {
       const int b0 = bb * 16, bw = min(16, w - b0);
+      // stage L[t0 + b0 + j][t0 + t] (t < b0 + bw, j < 16) as Ls[j * kLs + t] (Bs is free here)
+      for (int idx = tid; idx < 16 * (b0 + bw); idx += nw * 32) {
+        const int t = idx >> 4, j = idx & 15;
+        Bs[j * kLs + t] = j < bw ? Lr[(t0 + b0 + j) + (size_t)(t0 + t) * c] : 0.0;
+      }
+      __syncthreads();
       if (wid == 0) {
         double acc16[16];
 #pragma unroll
@@ -404,7 +418,7 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
         for (int j = 15; j >= 0; --j) {
           if (j < bw) {
 #pragma unroll
-            for (int jj = 0; jj < j; ++jj) acc16[jj] -= Lr[(t0 + b0 + j) + (size_t)(t0 + b0 + jj) * c] * acc16[j];
+            for (int jj = 0; jj < j; ++jj) acc16[jj] -= Bs[j * kLs + b0 + jj] * acc16[j];
           }
         }
 #pragma unroll
@@ -416,7 +430,7 @@ __device__ void big_bwd(const double* __restrict__ Lr, int c, int s, int f, cons
         double v = Vs[t * kVs + lane];
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (j < bw) v -= Lr[(t0 + b0 + j) + (size_t)(t0 + t) * c] * Vs[(b0 + j) * kVs + lane];
+          if (j < bw) v -= Bs[j * kLs + t] * Vs[(b0 + j) * kVs + lane];
         Vs[t * kVs + lane] = v;
       }
       __syncthreads();
@@ -574,7 +588,7 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
     flush(NW - 1);
     if (s >= kBigS) {
       __syncthreads();
-      big_fwd(Lr, c, s, f, rowind + a.colptr[f] + s, X, Vs, tid, lane, wid, NW);
+      big_fwd(Lr, c, s, f, rowind + a.colptr[f] + s, X, Vs, Bs, tid, lane, wid, NW);
     } else {
       const int32_t* U = rowind + a.colptr[f] + s;
       double* zs = zslots + slot * 16 * kPanelW;
