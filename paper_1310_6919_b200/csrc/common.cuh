@@ -60,6 +60,16 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return y;
 }
 
+// 1/d for a positive normal d: MUFU seed (rcp.approx.f64) + two Newton steps (r += r (1 - d r)).
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }

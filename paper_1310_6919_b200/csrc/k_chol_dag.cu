@@ -46,16 +46,33 @@ constexpr int kGemmSmem = kStages * kBK * ((NB + 4) + (NB / 2 + 4));  // doubles
 // the diagonal of L^{-1}, the current 32 x 32 diagonal-block inverse as a full square (later the scratch
 // block of the in-place L^{-1})
 constexpr int kPackN = 32 * (132 + 100 + 68 + 36);
-constexpr int kPotrfSmem = kPackN + NB + 32 * 36 + 32;
-constexpr int kSmem = kGemmSmem > kPotrfSmem ? kGemmSmem : kPotrfSmem;
+constexpr int kPotrfSmem = kPackN + NB + 32 * 36 + 64;  // (col: two 32-double broadcast buffers)
 constexpr int kCtl = 32;         // uint32 stride between queue counters (one 128-byte line each)
 constexpr int kQ = 5;            // ready queues
+#ifndef SDPC_WCHOL_V2
+#define SDPC_WCHOL_V2 1
+#endif
+#ifndef SDPC_DAG_BLOCKED_TRSM
+#define SDPC_DAG_BLOCKED_TRSM 1
+#endif
+#ifndef SDPC_DAG_FUSED_DIAG
+#define SDPC_DAG_FUSED_DIAG SDPC_DAG_BLOCKED_TRSM
+#endif
 #ifndef SDPC_DAG_CHAIN_SMS
+#if SDPC_DAG_FUSED_DIAG
+#define SDPC_DAG_CHAIN_SMS 4
+#elif SDPC_DAG_BLOCKED_TRSM
+#define SDPC_DAG_CHAIN_SMS 3
+#else
 #define SDPC_DAG_CHAIN_SMS 2
+#endif
 #endif
 #ifndef SDPC_DAG_MAX_STEPS
 #define SDPC_DAG_MAX_STEPS 4
 #endif
+constexpr int kLX = 132;                                            // fused diagonal update: 16 staged columns
+constexpr int kPotrfAll = kPotrfSmem + (SDPC_DAG_FUSED_DIAG ? 16 * kLX : 0);  // (<= 112 KB: 2 CTAs per SM)
+constexpr int kSmem = kGemmSmem > kPotrfAll ? kGemmSmem : kPotrfAll;
 constexpr int kChainSms = SDPC_DAG_CHAIN_SMS;  // SMs whose CTAs run only the panel chain
 constexpr int kMaxSteps = SDPC_DAG_MAX_STEPS;  // an update task applies up to this many consecutive panel steps
 
@@ -69,7 +86,14 @@ struct Args {
   double* B;
   int64_t ld;
   int m, T;
-  double* Linv;          // [T][NB * NB] column-major L_kk^{-1} (upper part zero)
+  double* Linv;          // [T][NB * NB] column-major, zero above the diagonal.  SDPC_DAG_BLOCKED_TRSM:
+                         // "Lmix" = the 32 x 32 diagonal blocks hold D_p^{-1} (the inverses of L's
+                         // diagonal blocks), the blocks below hold L; otherwise L_kk^{-1}
+  unsigned* pflag;       // [T] or null: column blocks of L_kk published so far by POTRF(k) (the chain
+                         // TRSM(k + 1, k, *) is released when POTRF(k) starts and follows it block by block)
+  unsigned* tflag;       // [2 T] or null (SDPC_DAG_FUSED_DIAG): column blocks of L_{k+1,k} rows [64 r, 64 r + 64)
+                         // stored so far by TRSM(k + 1, k, r); POTRF(k + 1) is released when both start and
+                         // applies the step-k update of its tile itself, block by block
   unsigned* ctl;         // head[q] = ctl[q * kCtl], tail[q] = ctl[(kQ + q) * kCtl]; ctl[2 kQ kCtl + r] = chain SM r;
                          // ctl[(2 kQ + 1) kCtl + q] = tasks of queue q absorbed into earlier updates (never pushed)
   uint64_t* slots[5];    // ready queues (see qof)
@@ -92,6 +116,10 @@ __device__ __forceinline__ int64_t uidx(const Args& a, int k, int i, int j) {  /
   return a.koff[k] + r * (r + 1) / 2 + (j - k - 1);
 }
 __device__ __forceinline__ int need_t(int k) { return k > 0 ? 3 : 1; }
+// POTRF(k), k >= 1: the two halves of UPD(k, k, k - 1); fused: the starts of TRSM(k, k - 1, *) and UPD(k, k, k - 2, *)
+__device__ __forceinline__ int need_p(const Args& a, int k) {
+  return (SDPC_DAG_FUSED_DIAG && a.tflag) ? 2 + (k >= 2 ? 2 : 0) : 2;
+}
 __device__ __forceinline__ int need_u(int i, int j, int k) { return (i != j ? 3 : 2) + (k > 0 ? 1 : 0); }
 // Queue of a task.  The panel chain POTRF(k) -> TRSM(k+1, k, *) -> UPD(k+1, k+1, k, *) -> POTRF(k+1) is
 // the critical path; it runs on the CTAs of kChainSms elected SMs that take nothing else, so the
@@ -186,13 +214,16 @@ __device__ void notify(const Args& a, uint64_t task, int lane) {
   const int k = (int)((task >> 32) & 0xffff), i = (int)((task >> 16) & 0xffff), j = (int)(task & 0xffff);
   const int T = a.T;
   if (type == kPotrf) {
-    for (int x = lane; x < 2 * (T - k - 1); x += 32) {
+    const int x0 = (SDPC_DAG_BLOCKED_TRSM && a.pflag) ? 2 : 0;  // TRSM(k + 1, k, *): released at the POTRF's start
+    for (int x = x0 + lane; x < 2 * (T - k - 1); x += 32) {
       const int ii = k + 1 + (x >> 1), r = x & 1;
       dep(a, &a.cnt_t[2 * tidx(ii, k) + r], need_t(k), enc(kTrsm, r, k, ii, 0));
     }
   } else if (type == kTrsm) {
     // rows of L_ik are the A operand of UPD(i, j, k, *) for k < j <= i ...
-    for (int x = lane; x < 2 * (i - k); x += 32) {
+    // (fused: the diagonal tile's update UPD(k + 1, k + 1, k, *) is done by POTRF(k + 1))
+    const int xu0 = (SDPC_DAG_FUSED_DIAG && a.tflag && i == k + 1) ? 2 : 0;
+    for (int x = xu0 + lane; x < 2 * (i - k); x += 32) {
       const int jj = k + 1 + (x >> 1), h = x & 1;
       dep(a, &a.cnt_u[2 * uidx(a, k, i, jj) + h], need_u(i, jj, k), enc(kUpd, h, k, i, jj));
     }
@@ -200,10 +231,12 @@ __device__ void notify(const Args& a, uint64_t task, int lane) {
     for (int l = i + 1 + lane; l < T; l += 32)
       dep(a, &a.cnt_u[2 * uidx(a, k, l, i) + hh], need_u(l, i, k), enc(kUpd, hh, k, l, i));
   } else if (lane == 0) {
-    if (j > k + 1) {
+    if (SDPC_DAG_FUSED_DIAG && a.tflag && i == j && j == k + 2) {
+      dep(a, &a.cnt_p[j], need_p(a, j), enc(kPotrf, 0, j, j, j));
+    } else if (j > k + 1) {
       dep(a, &a.cnt_u[2 * uidx(a, k + 1, i, j) + hh], need_u(i, j, k + 1), enc(kUpd, hh, k + 1, i, j));
     } else if (i == j) {
-      dep(a, &a.cnt_p[k + 1], 2, enc(kPotrf, 0, k + 1, k + 1, k + 1));
+      dep(a, &a.cnt_p[k + 1], need_p(a, k + 1), enc(kPotrf, 0, k + 1, k + 1, k + 1));
     } else {
       dep(a, &a.cnt_t[2 * tidx(i, k + 1)], need_t(k + 1), enc(kTrsm, 0, k + 1, i, 0));
       dep(a, &a.cnt_t[2 * tidx(i, k + 1) + 1], need_t(k + 1), enc(kTrsm, 1, k + 1, i, 0));
@@ -352,6 +385,130 @@ __device__ __forceinline__ void run_upd(const Args& a, int k, int ns, int i, int
                           doff, i == j, NB * ns, sm);
 }
 
+#if SDPC_DAG_BLOCKED_TRSM
+// TRSM(i, k, r): rows [64 r, 64 r + 64) of tile (i, k) <- A L_kk^{-T}, by 32-column blocks against Lmix
+// (forward substitution over the blocks, P:711-713 type (i) Cholesky): X_p = (A_p - sum_{q<p} X_q L_pq^T)
+// D_p^{-T}.  Warp (wm, wn) owns rows 32 wm .. 32 wm + 31 of column block wn, in registers; X_p goes through
+// shared memory (double-buffered) as the A operand of the later blocks' updates; column block p of Lmix
+// (rows 32 p ..) is staged in shared memory per stage.  The chain TRSM (i == k + 1, a.pflag set) waits
+// before stage p until POTRF(k) has published column block p, so it runs alongside its POTRF.
+__device__ __forceinline__ void run_trsm(const Args& a, int k, int i, int r, double* sm) {
+  constexpr int LX = 68, LL = 132;  // conflict-free fragment loads
+  __shared__ int s_stop;
+  const int64_t ri = (int64_t)i * NB + r * 64, ck = (int64_t)k * NB;
+  const int na = a.m - ri < 64 ? (int)(a.m - ri) : 64;
+  double* Ap = a.B + ri + ck * a.ld;
+  const double* Lm = a.Linv + (int64_t)k * NB * NB;
+  double* Xs = sm;             // [2][32 columns][LX]: X_p column-major, rows 0..63
+  double* Ls = sm + 2 * 32 * LX;  // [32 columns][LL]: rows 32 p .. 127 of column block p of Lmix
+  const bool early = a.pflag != nullptr && i == k + 1;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wm = wid & 1, wn = wid >> 1;
+  if (SDPC_DAG_FUSED_DIAG && early && a.tflag && tid == 0) {  // POTRF(k + 1) follows this TRSM block by block
+    dep(a, &a.cnt_p[k + 1], need_p(a, k + 1), enc(kPotrf, 0, k + 1, k + 1, k + 1));
+    if (na <= 0) {  // no rows (ragged last tile): nothing for POTRF(k + 1) to wait for
+      __threadfence();
+      atomicExch(a.tflag + 2 * k + r, 4u);
+    }
+  }
+  if (na <= 0) return;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int row = 32 * wm + 8 * x + g8;
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 32 * wn + 8 * y + 2 * t4 + e;
+        acc[x][y][e] = row < na ? __ldcg(Ap + row + (int64_t)col * a.ld) : 0.0;
+      }
+  }
+#pragma unroll 1
+  for (int p = 0; p < 4; ++p) {
+    if (early) {
+      if (tid == 0) {
+        unsigned spin = 0;
+        while (ld_vol(a.pflag + k) < (unsigned)(p + 1) && *(const volatile int32_t*)a.err == kNoError)
+          __nanosleep(spin++ < 16 ? 20 : 64);
+        __threadfence();  // acquire: column block p of Lmix is visible
+        s_stop = *(const volatile int32_t*)a.err != kNoError;
+      }
+    }
+    __syncthreads();  // (also: every warp is done with the previous stage's Ls)
+    if (early && s_stop) return;
+    // column block p of Lmix, rows 32 p .. 127, into Ls (16-byte cp.async, pairs of rows)
+    const int nrow2 = (NB - 32 * p) / 2;
+    for (int c = tid; c < 32 * nrow2; c += kThreads) {
+      const int col = c / nrow2, rr = 2 * (c % nrow2);
+      cp_async16(Ls + rr + col * LL, Lm + (32 * p + rr) + (int64_t)(32 * p + col) * NB, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    double* X = Xs + (p & 1) * 32 * LX;
+    if (wn == p) {
+      // X_p = acc D_p^{-T}: acc to shared as the A operand, then B(kk, n) = D_p^{-1}[n][kk] from Ls
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            X[(8 * y + 2 * t4 + e) * LX + 32 * wm + 8 * x + g8] = acc[x][y][e];
+            acc[x][y][e] = 0.0;
+          }
+      __syncwarp();
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) af[x] = X[(4 * k4 + t4) * LX + 32 * wm + 8 * x + g8];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) bf[y] = Ls[(8 * y + g8) + (4 * k4 + t4) * LL];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const int row = 32 * wm + 8 * x + g8;
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cl = 8 * y + 2 * t4 + e;
+            X[cl * LX + row] = acc[x][y][e];
+            if (row < na) __stcg(Ap + row + (int64_t)(32 * p + cl) * a.ld, acc[x][y][e]);
+          }
+      }
+    }
+    __syncthreads();
+    if (SDPC_DAG_FUSED_DIAG && early && a.tflag && tid == 0) {  // column block p of these rows is stored
+      __threadfence();
+      atomicExch(a.tflag + 2 * k + r, (unsigned)(p + 1));
+    }
+    if (wn > p) {
+      // acc -= X_p L_{wn,p}^T: B(kk, n) = L[32 wn + n][32 p + kk] at Ls row 32 (wn - p) + n
+#pragma unroll
+      for (int k4 = 0; k4 < 8; ++k4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) af[x] = neg(X[(4 * k4 + t4) * LX + 32 * wm + 8 * x + g8]);
+#pragma unroll
+        for (int y = 0; y < 4; ++y) bf[y] = Ls[(32 * (wn - p) + 8 * y + g8) + (4 * k4 + t4) * LL];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+      }
+    }
+  }
+}
+#else
 __device__ __forceinline__ void run_trsm(const Args& a, int k, int i, int r, double* sm) {
   const int64_t ri = (int64_t)i * NB + r * 64, ck = (int64_t)k * NB;
   const int na = a.m - ri < 64 ? (int)(a.m - ri) : 64;
@@ -359,6 +516,7 @@ __device__ __forceinline__ void run_trsm(const Args& a, int k, int i, int r, dou
   double* Ap = a.B + ri + ck * a.ld;
   tile_gemm<64, NB, false>(Ap, a.ld, a.Linv + (int64_t)k * NB * NB, NB, Ap, a.ld, na, NB, 0, false, NB, sm);
 }
+#endif
 
 // ------------------------------------------------------------------ POTRF task
 __device__ __forceinline__ int pofs(int p) { return 32 * (132 * p - 16 * p * (p - 1)); }
@@ -387,9 +545,40 @@ __device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double
   double row[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) row[c] = c <= lane ? Ab[lane + c * ld] : 0.0;
-  const double2* col2 = reinterpret_cast<const double2*>(col);
   int fail = -1;
   double rinv = 0.0;
+#if SDPC_WCHOL_V2
+  // The critical chain per column is pivot (shuffle) -> 1/d (MUFU seed + two Newton FMAs) -> multiplier
+  // -> update of the next pivot.  The column goes out UNSCALED (a_kj, independent of the pivot's
+  // reciprocal), so its shared-memory round trip overlaps the reciprocal: a_ik -= (a_ij / d_j) a_kj.
+  // The two broadcast buffers alternate (one warp barrier per column); 1/sqrt(d_j) scales row j's L
+  // entry off the chain.
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double d = shfl_d(row[j], j);
+    fail = (fail < 0 && !(d > 0.0)) ? j : fail;
+    double* cb = col + 32 * (j & 1);
+    if (j < 31) cb[lane] = row[j];
+    const double r = rcp_nr(d);
+    const double rl = rsqrt_nr(d);
+    rinv = lane == j ? rl : rinv;
+    if (j < 31) {
+      __syncwarp();
+      const double s = row[j] * r;
+      const double2* col2 = reinterpret_cast<const double2*>(cb);
+      // lanes < k update entries above the diagonal, which are never read
+#pragma unroll
+      for (int k2 = (j + 1) / 2; k2 < 16; ++k2) {
+        const double2 c = col2[k2];
+        if (2 * k2 > j) row[2 * k2] = fma(-s, c.x, row[2 * k2]);
+        row[2 * k2 + 1] = fma(-s, c.y, row[2 * k2 + 1]);
+      }
+    }
+    row[j] *= rl;
+  }
+  __syncwarp();
+#else
+  const double2* col2 = reinterpret_cast<const double2*>(col);
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const double d = shfl_d(row[j], j);
@@ -410,6 +599,7 @@ __device__ __forceinline__ int wchol32(double* Ab, int ld, double* ldiag, double
       __syncwarp();
     }
   }
+#endif
   if (fail >= 0) return fail;
   double dl = 0.0;
 #pragma unroll
@@ -476,6 +666,11 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
   const int g8 = lane >> 2, t4 = lane & 3;
   unsigned long long* pt = a.ptrace ? a.ptrace + 16 * k : nullptr;
   if (pt && tid == 0) pt[0] = gtimer();
+  // Lmix column blocks are published for the TRSMs of the panel below (not for the last tile)
+  const bool publish = SDPC_DAG_BLOCKED_TRSM && !INV_ONLY && k + 1 < a.T;
+  double* Lmx = a.Linv + (int64_t)k * NB * NB;
+  if (publish && a.pflag && tid == 0)  // the chain TRSM(k + 1, k, *) follows this POTRF block by block
+    for (int r = 0; r < 2; ++r) dep(a, &a.cnt_t[2 * tidx(k + 1, k) + r], need_t(k), enc(kTrsm, r, k, k + 1, 0));
   // the lower tile into the packed panels by 16-byte cp.async (pairs of rows of one column); chunks
   // entirely above the diagonal or outside the kb x kb tile are zero-filled
   for (int c = tid; c < 16 * (128 + 96 + 64 + 32); c += kThreads) {
@@ -495,6 +690,97 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
   __syncthreads();
   for (int i = kb + tid; i < NB; i += kThreads) *pel(S, i, i) = 1.0;  // identity padding of a ragged tile
   __syncthreads();
+#if SDPC_DAG_FUSED_DIAG
+  if (!INV_ONLY && a.tflag && k >= 1) {
+    // The step-(k-1) update of this diagonal tile, C -= L_{k,k-1} L_{k,k-1}^T, applied here (no separate
+    // UPD task on the chain), 16 columns of L_{k,k-1} at a time as TRSM(k, k-1, *) stores them.  The
+    // K-sum is accumulated from zero and subtracted once (as the diagonal update tasks do).  Warps 0-5:
+    // the off-diagonal 32 x 32 blocks (I, J); warps 6, 7: the lower 8 x 8 tiles of two diagonal blocks each.
+    __shared__ int s_stop2;
+    if (pt && tid == 0) pt[9] = gtimer();
+    const double* X = a.B + k0 + (int64_t)(k0 - NB) * a.ld;  // tile (k, k - 1)
+    double* Xst = sm + kPotrfSmem;                          // [16 columns][kLX], rows 0..127
+    const bool offd = wid < 6;
+    const int bI = offd ? (wid < 3 ? wid + 1 : (wid < 5 ? wid - 1 : 3)) : (wid == 6 ? 0 : 1);
+    const int bJ = offd ? (wid < 3 ? 0 : (wid < 5 ? 1 : 2)) : (wid == 6 ? 3 : 2);  // diag warps: 2nd block
+    double acc[20][2];
+#pragma unroll
+    for (int t = 0; t < 20; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll 1
+    for (int hs = 0; hs < 8; ++hs) {
+      if ((hs & 1) == 0 && tid == 0) {
+        const unsigned want = (unsigned)(hs / 2 + 1);
+        const unsigned* f = a.tflag + 2 * (k - 1);
+        unsigned spin = 0;
+        while ((ld_vol(f) < want || ld_vol(f + 1) < want) && *(const volatile int32_t*)a.err == kNoError)
+          __nanosleep(spin++ < 16 ? 20 : 64);
+        __threadfence();  // acquire: the block's columns are visible
+        s_stop2 = *(const volatile int32_t*)a.err != kNoError;
+      }
+      __syncthreads();  // (also: the previous half-slice is consumed)
+      if (s_stop2) return;
+      for (int c = tid; c < 16 * (NB / 2); c += kThreads) {
+        const int col = c / (NB / 2), rr = 2 * (c % (NB / 2));
+        const int bytes = rr + 1 < kb ? 16 : (rr < kb ? 8 : 0);  // rows beyond the matrix: zeros
+        cp_async16_n(Xst + rr + col * kLX, bytes ? X + rr + (int64_t)(16 * hs + col) * a.ld : X, bytes);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const double* xr = Xst + (4 * k4 + t4) * kLX + g8;
+        if (offd) {
+          double af[4], bf[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) af[x] = xr[32 * bI + 8 * x];
+#pragma unroll
+          for (int y = 0; y < 4; ++y) bf[y] = xr[32 * bJ + 8 * y];
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[4 * x + y][0], acc[4 * x + y][1], af[x], bf[y]);
+        } else {
+          double f0[4], f1[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            f0[x] = xr[32 * bI + 8 * x];
+            f1[x] = xr[32 * bJ + 8 * x];
+          }
+          int t = 0;
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y <= x; ++y, ++t) {
+              dmma_8x8x4(acc[t][0], acc[t][1], f0[x], f0[y]);
+              dmma_8x8x4(acc[10 + t][0], acc[10 + t][1], f1[x], f1[y]);
+            }
+        }
+      }
+    }
+    // C -= acc in the packed tile (diagonal 8 x 8 tiles: the entries above their diagonal are never read)
+    if (offd) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) *pel(S, 32 * bI + 8 * x + g8, 32 * bJ + 8 * y + 2 * t4 + e) -= acc[4 * x + y][e];
+    } else {
+      int t = 0;
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y <= x; ++y, ++t)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            *pel(S, 32 * bI + 8 * x + g8, 32 * bI + 8 * y + 2 * t4 + e) -= acc[t][e];
+            *pel(S, 32 * bJ + 8 * x + g8, 32 * bJ + 8 * y + 2 * t4 + e) -= acc[10 + t][e];
+          }
+    }
+    __syncthreads();
+  }
+#endif
   if (pt && tid == 0) pt[1] = gtimer();
 #pragma unroll 1
   for (int p = 0; p < 4; ++p) {
@@ -516,7 +802,25 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
     }
     if (pt && tid == 0) pt[2 + p] = gtimer();
     const int r0 = c0 + 32, nr = NB - r0;
-    if (nr == 0) break;
+    // column block p of Lmix (rows 32 p .. 127): D_p^{-1} (row b, column a of the diagonal block holds
+    // D_p^{-1}[a][b]) and L below; then released to the waiting TRSMs
+    auto publish_block = [&]() {
+      for (int x = tid; x < 32 * (NB - c0); x += kThreads) {
+        const int jc = x / (NB - c0), i = c0 + x % (NB - c0);
+        const int ic = i - c0;
+        const double v = ic < 32 ? (ic >= jc ? P[jc + ic * ldp] : 0.0) : P[ic + jc * ldp];
+        __stcg(Lmx + i + (int64_t)(c0 + jc) * NB, v);
+      }
+      __syncthreads();
+      if (a.pflag && tid == 0) {
+        __threadfence();
+        atomicExch(a.pflag + k, (unsigned)(p + 1));
+      }
+    };
+    if (nr == 0) {
+      if (publish) publish_block();
+      break;
+    }
     // panel rows below the diagonal block, in place: X = A Dinv^T (one warp per 8-row strip)
     for (int tr = wid; tr < nr / 8; tr += kThreads / 32) {
       double* Ar = P + (r0 + tr * 8 - c0);
@@ -534,6 +838,7 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
       }
     }
     __syncthreads();
+    if (publish) publish_block();
     // trailing update A22 -= X X^T on the 8 x 8 tiles (ti >= tj) of rows / columns r0..127; tiles are
     // dealt to the warps round-robin in row-major order
     const int nb8 = nr / 8;
@@ -571,7 +876,10 @@ __device__ void run_potrf(const Args& a, int k, double* sm) {
     for (int i = j + lane; i < kb; i += 32) __stcg(Bd + i + (int64_t)j * a.ld, i == j ? ldiag[i] : col[i]);
   }
   if (pt && tid == 0) pt[6] = gtimer();
-  if (!INV_ONLY && k == a.T - 1) return;  // no panel below the last tile: its inverse is not needed
+  if (!INV_ONLY && (SDPC_DAG_BLOCKED_TRSM || k == a.T - 1)) {
+    if (pt && tid == 0) pt[7] = pt[8] = gtimer();
+    return;
+  }  // (Lmix is published; the last tile has no panel below)
   // L^{-1} in shared memory, in place by block rows I = 1..3 and columns J < I (ascending):
   //   T = sum_{K=J}^{I-1} L[I,K] Linv[K,J]  (L[I,K] for K >= J is still L: only columns < J of row I are
   //   overwritten yet);  Linv[I,J] = -Dinv_I T  replaces L[I,J] (panel J, rows 32 I ..).
@@ -850,7 +1158,7 @@ static DagSizes dag_sizes(int T) {
   DagSizes s;
   for (int k = 0; k < T; ++k) s.nu += (int64_t)(T - k - 1) * (T - k) / 2;
   s.nt = (int64_t)T * (T - 1) / 2;
-  s.total = T + 2 * s.nt + 2 * s.nu;
+  s.total = T + 2 * s.nt + 2 * s.nu - (SDPC_DAG_FUSED_DIAG ? 2 * (int64_t)std::max(0, T - 1) : 0);  // (fused: no UPD(k+1, k+1, k, *))
   int64_t c1 = 0, c2 = 0;  // tiles of the next panel's column / the column after, over all steps
   for (int k = 0; k < T; ++k) {
     c1 += std::max(0, T - k - 1);
@@ -858,12 +1166,12 @@ static DagSizes dag_sizes(int T) {
   }
   const int64_t chain = 4 * (int64_t)std::max(0, T - 1);  // TRSM(k+1, k, *) + UPD(k+1, k+1, k, *)
   s.q_n[0] = T;
-  s.q_n[1] = chain;
+  s.q_n[1] = SDPC_DAG_FUSED_DIAG ? chain / 2 : chain;
   s.q_n[2] = 2 * s.nt + 2 * c1 - chain;
   s.q_n[3] = 2 * c2;
   s.q_n[4] = s.total - s.q_n[0] - s.q_n[1] - s.q_n[2] - s.q_n[3];
   s.ctl_b = (2 * dag::kQ * dag::kCtl + 2 * dag::kCtl) * 4;
-  s.cnt_b = 4 * ((int64_t)T + 2 * s.nt + 2 * s.nu);
+  s.cnt_b = 4 * ((int64_t)T + 2 * s.nt + 2 * s.nu + 3 * T);  // (+ T: pflag, + 2 T: tflag)
   return s;
 }
 
@@ -919,6 +1227,8 @@ int potrf_dag(sdpc_ctx* h, double* B, int64_t m, int64_t ld, int32_t* d_err, cud
   a.cnt_p = cnt;
   a.cnt_t = cnt + T;
   a.cnt_u = cnt + T + 2 * s.nt;
+  a.pflag = SDPC_DAG_BLOCKED_TRSM ? reinterpret_cast<unsigned*>(cnt + T + 2 * s.nt + 2 * s.nu) : nullptr;
+  a.tflag = SDPC_DAG_FUSED_DIAG ? reinterpret_cast<unsigned*>(cnt + 2 * T + 2 * s.nt + 2 * s.nu) : nullptr;
   uint64_t* q = reinterpret_cast<uint64_t*>(base + s.ctl_b + ((s.cnt_b + 7) / 8) * 8);
   for (int x = 0; x < kQ; ++x) {
     a.slots[x] = q;

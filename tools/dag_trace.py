@@ -89,6 +89,9 @@ ps, pe = t0[pot] / 1e3, t1[pot] / 1e3
 gaps = ps[1:] - pe[:-1]
 print(f"POTRF chain: first start {ps[0]:.1f} us, last end {pe[-1]:.1f} us; POTRF-to-next-POTRF gap mean {gaps.mean():.1f} us"
       f" p50 {np.median(gaps):.1f} max {gaps.max():.1f}")
+ends = np.diff(pe)
+print(f"chain step (POTRF end to next POTRF end): mean over the last 30 steps {ends[-30:].mean():.1f} us, "
+      f"last 40 {ends[-40:].mean():.1f} us, all {ends.mean():.1f} us")
 for kk in list(range(0, len(pot), max(1, len(pot) // 12))):
     print(f"  k={kk:4d} potrf [{ps[kk]:9.1f}, {pe[kk]:9.1f}] us")
 # utilisation over time (10 bins)
