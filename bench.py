@@ -269,7 +269,9 @@ def run_ours(args, rank, world, local_rank):
         "note": ("(b): SURVEY 8(d) flops per RHS (etree-reach forward + backward over nnz(E[p:,p:]) when "
                  "max-cut truncation is on, + D scaling) over the solved RHS, per launch window (the X-hat "
                  "window overlaps (a2)); FP64 roof = the line's peak.  (c): B lower triangle written once "
-                 "(8 m(m+1)/2 bytes) over the accumulate kernel; HBM roof = MEASURED_PEAKS hbm_gbs.  (d): m^3/3 "
+                 "(8 m(m+1)/2 bytes) over the accumulate kernel; HBM roof = MEASURED_PEAKS hbm_gbs; "
+                 "*_with_panel_reads adds the one read of the materialised truncated X-hat / Y^-1 panels the "
+                 "unfused kernel needs (ncu: profiles/r02/ncu/scm_c1_full.txt, 0.99 GB read + 0.45 GB written).  (d): m^3/3 "
                  "over the Cholesky kernel."),
     }
     for key in ("b_solve_x", "b_solve_y", "d_cholesky"):
@@ -277,6 +279,12 @@ def run_ours(args, rank, world, local_rank):
         phase_roof[key]["frac_fp64"] = v / fp64_peak_tf if v else None
     gbs = phase_roof["c_accumulate"]["gbs"]
     phase_roof["c_accumulate"]["frac_hbm"] = gbs / pk["hbm"] if gbs else None
+    if inst.kind == "maxcut" and kt[2] > 0:
+        # the unfused kernel also reads the materialised X-hat / Y^-1 panels once: rows i >= v of column v
+        # (max-cut truncation), two arrays -> 2 * 8 * n(n+1)/2 bytes on top of the B write
+        pbytes = bbytes + 2 * 8.0 * entries(inst.n)
+        phase_roof["c_accumulate"]["bytes_with_panel_reads"] = pbytes
+        phase_roof["c_accumulate"]["frac_hbm_with_panel_reads"] = pbytes / (kt[2] * 1e-3) / 1e9 / pk["hbm"]
     value = world * entries(m) / (ms * 1e-3)
     line = {
         "metric": METRIC,

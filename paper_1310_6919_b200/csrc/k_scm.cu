@@ -7,8 +7,10 @@
 // Only columns p, q of A_l are read (X-hat e_p, Y^{-1} e_q: the paper's x_p and v = Y^{-1}[A_l]_{*p}),
 // so a rank that holds the columns l of B it builds needs only those RHS.
 //  * max-cut (every A_k = a_k e_{v_k} e_{v_k}^T, distinct v_k): B_kl = a_k a_l X-hat_{v_k v_l} Y^{-1}_{v_k v_l},
-//    i.e. B = X-hat o Y^{-1} (SURVEY §8(c) pins).  One thread per row k reads whole
-//    256-byte panel rows of both inverses and writes 32 columns of B.
+//    i.e. B = X-hat o Y^{-1} (SURVEY §8(c) pins).  Full solves (multi-rank): one thread per
+//    row k reads whole 256-byte panel rows of both inverses and writes 32 columns of B; truncated
+//    solves (one rank): one warp per 32 rows x one panel, coalesced row reads, transposed through
+//    shared memory (scm_maxcut_trunc_kernel).
 //  * general: one thread per (k, l); A_l's entries staged in shared memory.
 //  * "large" constraints (many entries, e.g. A_1 = I of the theta SDP): one CTA per (K, l) pair
 //    with a block reduction over the entry-pair product (SURVEY: warp-shuffle reductions).
@@ -28,7 +30,6 @@ __device__ __forceinline__ double pm(const double* __restrict__ M, const int32_t
   return M[((size_t)(s >> 5) * n + row) * kPanelW + (s & 31)];
 }
 
-template <bool TRUNC>
 __global__ void __launch_bounds__(256) scm_maxcut_kernel(int n, int m, const double* __restrict__ Xh,
                                                          const double* __restrict__ Yh,
                                                          const int32_t* __restrict__ rhs,
@@ -54,31 +55,65 @@ __global__ void __launch_bounds__(256) scm_maxcut_kernel(int n, int m, const dou
   double* Bk = B + g.lrow(k);
   const double2* xr = reinterpret_cast<const double2*>(Xh + ((size_t)P * n + i) * kPanelW);
   const double2* yr = reinterpret_cast<const double2*>(Yh + ((size_t)P * n + i) * kPanelW);
-  if (TRUNC) {
-    // truncated solves: column v of the panel is valid at rows i >= v only; the pair {k, l} is taken
-    // from the panel of the smaller elimination index and written to the lower triangle of B
-    if (i < lvtx[0] || lvtx[0] < 0) return;
-#pragma unroll 4
-    for (int h = 0; h < kPanelW / 2; ++h) {
-      const double2 x = xr[h], y = yr[h];
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = 2 * h + e, l = lcol[c];
-        if (l >= 0 && i >= lvtx[c]) {
-          const double v = ak * lval[c] * (e ? x.y : x.x) * (e ? y.y : y.x);
-          if (k >= l) B[k + (size_t)l * ldb] = v;
-          else B[l + (size_t)k * ldb] = v;
-        }
-      }
-    }
-    return;
-  }
 #pragma unroll 4
   for (int h = 0; h < kPanelW / 2; ++h) {
     const double2 x = xr[h], y = yr[h];
     const int l0 = lcol[2 * h], l1 = lcol[2 * h + 1];
     if (l0 >= 0 && k >= l0) Bk[g.lcol(l0) * ldb] = ak * lval[2 * h] * x.x * y.x;
     if (l1 >= 0 && k >= l1) Bk[g.lcol(l1) * ldb] = ak * lval[2 * h + 1] * x.y * y.y;
+  }
+}
+
+// Max-cut with truncated solves (one rank): column v of the panel is valid at rows i >= v only; the pair
+// {k, l} is taken from the panel of the smaller elimination index and written to the lower triangle of B.
+// One warp per 32 consecutive constraints k and one panel: the 32 panel rows vrow[k] of X-hat and Y^{-1}
+// are read as whole 256-byte rows (lane = panel column, two L1 wavefronts per load instead of the 32 of a
+// thread-per-row double2 walk), the products go through a padded per-warp shared square and are written
+// with lane = k, so the k >= l stores are 256-byte runs of a column of B.
+constexpr int kTruncWarps = 4;
+__global__ void __launch_bounds__(kTruncWarps * 32) scm_maxcut_trunc_kernel(
+    int n, int m, const double* __restrict__ Xh, const double* __restrict__ Yh, const int32_t* __restrict__ rhs,
+    const int32_t* __restrict__ vrow, const double* __restrict__ aval, const int32_t* __restrict__ col_cons,
+    double* B, int64_t ldb) {
+  __shared__ int32_t lcol[kPanelW], lvtx[kPanelW];
+  __shared__ double lval[kPanelW];
+  __shared__ double tile[kTruncWarps][kPanelW][kPanelW + 1];
+  const int P = blockIdx.y;
+  if (threadIdx.x < kPanelW) {
+    const int v = rhs[P * kPanelW + threadIdx.x];
+    const int l = v >= 0 ? col_cons[v] : -1;
+    lcol[threadIdx.x] = l;
+    lvtx[threadIdx.x] = v;
+    lval[threadIdx.x] = l >= 0 ? aval[l] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int k = (blockIdx.x * kTruncWarps + wid) * 32 + lane;
+  const int v0 = lvtx[0];
+  if (v0 < 0) return;
+  const int i = k < m ? vrow[k] : -1;
+  const double ak = k < m ? aval[k] : 0.0;
+  if (!__any_sync(0xffffffffu, i >= v0)) return;
+  const double lv = lval[lane];
+  const double* xp = Xh + (size_t)P * n * kPanelW + lane;
+  const double* yp = Yh + (size_t)P * n * kPanelW + lane;
+  double(*T)[kPanelW + 1] = tile[wid];
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) {
+    const int ir = __shfl_sync(0xffffffffu, i, r);
+    const double ar = __shfl_sync(0xffffffffu, ak, r);
+    if (ir >= v0) T[r][lane] = ar * lv * __ldg(xp + (size_t)ir * kPanelW) * __ldg(yp + (size_t)ir * kPanelW);
+  }
+  __syncwarp();
+  if (i < v0) return;
+#pragma unroll 4
+  for (int c = 0; c < kPanelW; ++c) {
+    const int l = lcol[c];
+    if (l >= 0 && i >= lvtx[c]) {
+      const double v = T[lane][c];
+      if (k >= l) B[k + (size_t)l * ldb] = v;
+      else B[l + (size_t)k * ldb] = v;
+    }
   }
 }
 
@@ -291,10 +326,11 @@ int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st) {
     if (h->d.npanels == 0) return 0;
     dim3 grid((m + 255) / 256, h->d.npanels);
     if (h->trunc_active)
-      scm_maxcut_kernel<true><<<grid, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B, ldb,
-                                                     g);
+      scm_maxcut_trunc_kernel<<<dim3((m + kTruncWarps * 32 - 1) / (kTruncWarps * 32), h->d.npanels),
+                                kTruncWarps * 32, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B,
+                                                           ldb);
     else
-      scm_maxcut_kernel<false><<<grid, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B,
+      scm_maxcut_kernel<<<grid, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.rhs, c.vrow, c.aval, c.col_cons, B,
                                                       ldb, g);
     return 1;
   }
