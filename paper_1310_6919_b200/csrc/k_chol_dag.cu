@@ -67,6 +67,9 @@ constexpr int kQ = 5;            // ready queues
 #define SDPC_DAG_CHAIN_SMS 2
 #endif
 #endif
+#ifndef SDPC_DAG_FRAG_PIPE  // explicit fragment double-buffering (volatile LDS): configs[1] 15.35 -> 15.30 ms, not kept
+#define SDPC_DAG_FRAG_PIPE 0
+#endif
 #ifndef SDPC_DAG_MAX_STEPS
 #define SDPC_DAG_MAX_STEPS 4
 #endif
@@ -338,6 +341,33 @@ __device__ __forceinline__ void tile_gemm(const double* A, int64_t lda, const do
     cp_async_commit();
     const double* as = As + (kc % kStages) * kBK * LA;
     const double* bs = Bs + (kc % kStages) * kBK * LB;
+#if SDPC_DAG_FRAG_PIPE
+    // fragments of step k4 + 1 are loaded before the DMMAs of step k4 are issued (two register sets):
+    // without this the compiler loads each B fragment right before the four DMMAs that use it
+    double af[2][4], bf[2][4];
+    const unsigned as_u = (unsigned)__cvta_generic_to_shared(as + t4 * LA + wm * 32 + g8);
+    const unsigned bs_u = (unsigned)__cvta_generic_to_shared(bs + t4 * LB + wn * 32 + g8);
+    auto ldfrag = [&](int buf, int k4) {  // volatile loads: kept in this order relative to the DMMAs
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        double v;
+        asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(as_u + (unsigned)((k4 * 4 * LA + x * 8) * 8)));
+        af[buf][x] = UPD ? neg(v) : v;
+      }
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+        asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(bf[buf][y]) : "r"(bs_u + (unsigned)((k4 * 4 * LB + y * 8) * 8)));
+    };
+    ldfrag(0, 0);
+#pragma unroll
+    for (int k4 = 0; k4 < kBK / 4; ++k4) {
+      if (k4 + 1 < kBK / 4) ldfrag((k4 + 1) & 1, k4 + 1);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[k4 & 1][x], bf[k4 & 1][y]);
+    }
+#else
 #pragma unroll
     for (int k4 = 0; k4 < kBK / 4; ++k4) {
       double af[4], bf[4];
@@ -353,6 +383,7 @@ __device__ __forceinline__ void tile_gemm(const double* A, int64_t lda, const do
 #pragma unroll
         for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
     }
+#endif
     if (cadd && (kc + 1) % (NB / kBK) == 0 && kc + 1 < nk) flush_c();
   }
   cp_async_wait<0>();

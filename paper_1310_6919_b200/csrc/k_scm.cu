@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) scm_general_kernel(int n, int m, const do
 // (coalesced), then every B_kl, k >= l, is sum_e v_e sum_f w_f Xr[p_f][j_e] Yr[q_f][i_e] with
 // shared-memory reads only; the entries (K, l) with K a diagonal-only large constraint (A_1 = I of
 // the theta SDP) are the block reductions sum_f w_f sum_t wK[t] Xr[p_f][t] Yr[q_f][t].
-__global__ void __launch_bounds__(256) scm_rows_kernel(int n, int m, const double* __restrict__ Xh,
+__global__ void __launch_bounds__(1024) scm_rows_kernel(int n, int m, const double* __restrict__ Xh,
                                                        const double* __restrict__ Yh,
                                                        const int64_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ ei,
@@ -176,21 +176,32 @@ __global__ void __launch_bounds__(256) scm_rows_kernel(int n, int m, const doubl
   extern __shared__ double rows_sm[];
   __shared__ int32_t sp[kMaxSmall], sq[kMaxSmall];
   __shared__ double sw[kMaxSmall];
-  __shared__ double red[8];
+  __shared__ double red[32];
   const int l = blockIdx.x;
   if (is_large[l]) return;
   const int nv = vptr[l + 1] - vptr[l];
   double* Xr = rows_sm;             // [nv][n]
   double* Yr = rows_sm + (size_t)nv * n;
   const int tid = threadIdx.x;
+  // rows are staged by cp.async (no register round trip: every thread has all its copies in flight);
+  // 16-byte copies when n is even (row starts in shared memory stay 16-byte aligned)
   for (int a = 0; a < nv; ++a) {
     const int v = vlist[vptr[l] + a];
-    for (int t = tid; t < n; t += blockDim.x) {
-      const size_t o = ((size_t)(t >> 5) * n + v) * kPanelW + (t & 31);
-      Xr[(size_t)a * n + t] = Xh[o];
-      Yr[(size_t)a * n + t] = Yh[o];
+    if ((n & 1) == 0) {
+      for (int t = 2 * tid; t < n; t += 2 * blockDim.x) {
+        const size_t o = ((size_t)(t >> 5) * n + v) * kPanelW + (t & 31);
+        cp_async16(Xr + (size_t)a * n + t, Xh + o, true);
+        cp_async16(Yr + (size_t)a * n + t, Yh + o, true);
+      }
+    } else {
+      for (int t = tid; t < n; t += blockDim.x) {
+        const size_t o = ((size_t)(t >> 5) * n + v) * kPanelW + (t & 31);
+        cp_async8(Xr + (size_t)a * n + t, Xh + o, true);
+        cp_async8(Yr + (size_t)a * n + t, Yh + o, true);
+      }
     }
   }
+  cp_async_commit();
   const int64_t lb = ptr[l];
   const int nl = (int)(ptr[l + 1] - lb);
   for (int t = tid; t < nl; t += blockDim.x) {
@@ -198,6 +209,7 @@ __global__ void __launch_bounds__(256) scm_rows_kernel(int n, int m, const doubl
     sq[t] = eloc[2 * (lb + t) + 1];
     sw[t] = ev[lb + t];
   }
+  cp_async_wait<0>();
   __syncthreads();
   for (int k = l + tid; k < m; k += blockDim.x) {
     if (is_large[k]) continue;
@@ -340,7 +352,8 @@ int launch_scm(sdpc_ctx* h, double* B, int64_t ldb, cudaStream_t st) {
     static std::atomic<uint64_t> attr{0};
     if (once_per_device(attr))
       cudaFuncSetAttribute(scm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowsSmemCap);
-    scm_rows_kernel<<<m, 256, smem, st>>>(n, m, h->Xh, h->Yh, c.ptr, c.ei, c.ej, c.ev, c.is_large, c.vptr, c.vlist,
+    // one or two CTAs fit an SM when the staged rows are big: more warps per CTA hide the gather latency
+    scm_rows_kernel<<<m, smem > 48 * 1024 ? 1024 : 256, smem, st>>>(n, m, h->Xh, h->Yh, c.ptr, c.ei, c.ej, c.ev, c.is_large, c.vptr, c.vlist,
                                           c.eloc, c.wdiag, c.dlist, c.ndiag, B, ldb);
   } else {
     scm_general_kernel<<<m, 256, 0, st>>>(n, m, h->Xh, h->Yh, h->d.slot_of, c.ptr, c.ei, c.ej, c.ev, c.is_large, B,
