@@ -214,6 +214,23 @@ __device__ int cta_chol_partial(double* A, int c, int ncols, const Scratch& s, i
   return -1;
 }
 
+// inverse of the 32 x 32 (jw valid) lower diagonal block M[J,J] at row jb, lane = column, into dst
+// (ld kLdInv): one warp.  It does not depend on W, so the back substitution runs it one block ahead.
+__device__ __noinline__ void warp_tri_inv32(const double* A, int lda, int jb, int jw, double* dst) {
+  const int lane = threadIdx.x & 31;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double sacc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) sacc -= ((i < jw && k < jw) ? A[(jb + i) + (size_t)(jb + k) * lda] : 0.0) * x[k];
+    const double dii = (i < jw) ? A[(jb + i) + (size_t)(jb + i) * lda] : 1.0;
+    x[i] = sacc / dii;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) dst[i + lane * kLdInv] = i >= lane ? x[i] : 0.0;
+}
+
 // W (c x s, ld c) = M^{-T} [0; I_s]: blocked back substitution from the last 32-row block up.
 // M lower (A, ld c).  Column t of W is nonzero only in rows <= u + t.
 template <int NT>
@@ -225,20 +242,27 @@ __device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, 
     const int i = idx % c, t = idx / c;
     W[idx] = (i == u + t) ? 1.0 : 0.0;
   }
-  __syncthreads();
   const int nblk = (c + 31) / 32;
+  // warp 0 inverts the diagonal block of step bI - 1 (into the other of two buffers; sc.l11 is free
+  // after the Cholesky) while the other warps apply the DMMA update of step bI
+  double* ibuf[2] = {sc.inv, sc.l11};
+  constexpr int kUpdW = NT > 32 ? NT / 32 - 1 : 1;  // warps on the update
+  if (wid == 0) warp_tri_inv32(A, lda, (nblk - 1) * 32, min(32, c - (nblk - 1) * 32), ibuf[(nblk - 1) & 1]);
+  __syncthreads();
   for (int bI = nblk - 1; bI >= 0; --bI) {
     const int jb = bI * 32, jw = min(32, c - jb);
     const int t0 = jb > u ? jb - u : 0;  // columns t < t0 are zero in rows >= jb
     const int ns = s - t0;
     // W[J, t] -= sum_{i >= jb+jw} M[i, jb+q] W[i, t]
     const int lo = jb + jw;
-    if (lo < c && ns > 0) {
+    if (NT > 32 && wid == 0) {
+      if (bI > 0) warp_tri_inv32(A, lda, jb - 32, 32, ibuf[(bI - 1) & 1]);
+    } else if (lo < c && ns > 0) {
       // DMMA 8 x 8 tiles (q block x t block), K = c - lo; rows i > u + t of W are zero, so the
       // full K range adds nothing there
       const int g8 = lane >> 2, t4 = lane & 3;
       const int nq8 = (jw + 7) >> 3, nt8 = (ns + 7) >> 3, K = c - lo;
-      for (int task = wid; task < nq8 * nt8; task += NT / 32) {
+      for (int task = (NT > 32 ? wid - 1 : 0); task < nq8 * nt8; task += kUpdW) {
         const int qb = (task % nq8) * 8, tb = t0 + (task / nq8) * 8;
         const int qa = qb + g8, ta = tb + g8;
         const double* Ap = A + lo + (size_t)(jb + qa) * lda;
@@ -256,21 +280,8 @@ __device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, 
         if (q < jw && t + 1 < s) W[jb + q + (size_t)(t + 1) * c] -= c1;
       }
     }
-    // inverse of the diagonal block M[J,J] (lower): warp 0
-    if (wid == 0) {
-      double x[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        double sacc = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; ++k) sacc -= ((i < jw && k < jw) ? A[(jb + i) + (size_t)(jb + k) * lda] : 0.0) * x[k];
-        const double dii = (i < jw) ? A[(jb + i) + (size_t)(jb + i) * lda] : 1.0;
-        x[i] = sacc / dii;
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) sc.inv[i + lane * kLdInv] = i >= lane ? x[i] : 0.0;
-    }
     __syncthreads();
+    const double* binv = ibuf[bI & 1];
     // W[J, t] = M[J,J]^{-T} W[J, t]:  W_new[q] = sum_{p >= q} inv[p][q] W_old[p], one thread per column t
     for (int t = t0 + tid; t < s; t += NT) {
       double w[32];
@@ -281,7 +292,7 @@ __device__ void cta_backsub_last_rows(const double* A, double* W, int c, int s, 
         if (q < jw) {
           double acc = 0.0;
 #pragma unroll
-          for (int p = q; p < 32; ++p) acc += sc.inv[p + q * kLdInv] * w[p];
+          for (int p = q; p < 32; ++p) acc += binv[p + q * kLdInv] * w[p];
           W[jb + q + (size_t)t * c] = acc;
         }
       }
@@ -457,6 +468,10 @@ __global__ void __launch_bounds__(256) pre_extend_add_kernel(CliqueArgs a, const
 // tensor cores straight into the update-matrix storage.  Same arithmetic as mf_kernel,
 // with the Schur complement no longer streamed through a single SM.
 constexpr int kThinS = 32;  // fronts with at most this many pivots: front_thin_kernel
+#ifndef SDPC_PANEL_NT
+#define SDPC_PANEL_NT 512
+#endif
+constexpr int kPanelNT = SDPC_PANEL_NT;  // threads of front_panel_kernel (one CTA per front)
 
 template <int NT>
 __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int32_t* __restrict__ list, int pbytes) {
@@ -469,10 +484,25 @@ __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int
   double* F = a.ws + a.ws_off[r];
   const int tid = threadIdx.x;
   const int64_t* __restrict__ colptr = a.colptr;
-  for (int j = 0; j < s; ++j) {  // (2D loops: no 64-bit division per element)
-    const double* yc = a.vals + colptr[f + j] - j;
-    double* Fc = F + (size_t)j * c;
-    for (int i = j + tid; i < c; i += NT) Fc[i] += yc[i];
+  // Y's pivot columns into the front: a thread owns row i and takes 8 columns at a time, loads first
+  // (a column-by-column loop exposes one memory round trip per pivot column to the whole CTA)
+  {
+    const double* __restrict__ vals = a.vals;
+    for (int i = tid; i < c; i += NT) {
+      const int jm = min(i, s - 1);
+      for (int j0 = 0; j0 <= jm; j0 += 8) {
+        double y[8], fv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u <= jm) {
+            y[u] = vals[colptr[f + j0 + u] - (j0 + u) + i];
+            fv[u] = F[i + (size_t)(j0 + u) * c];
+          }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (j0 + u <= jm) F[i + (size_t)(j0 + u) * c] = fv[u] + y[u];
+      }
+    }
   }
   __syncthreads();
   double* panel = ((size_t)c * 32 * sizeof(double) <= (size_t)pbytes) ? smem : F + (size_t)c * c + (size_t)c * s;
@@ -482,13 +512,30 @@ __global__ void __launch_bounds__(NT) front_panel_kernel(CliqueArgs a, const int
     if (tid == 0) report_error(a.err, f + fail);
     return;
   }
-  double* Lp = a.Lp + a.panel_off[r];
-  for (int t = 0; t < s; ++t) {
-    const double dg = F[t + (size_t)t * c], rdg = 1.0 / dg;
-    const double* Fc = F + (size_t)t * c;
-    double* Lc = Lp + (size_t)t * c;
-    for (int ar = tid; ar < c; ar += NT) Lc[ar] = ar > t ? Fc[ar] * rdg : (ar == t ? 1.0 : 0.0);
-    if (tid == 0) a.D[f + t] = dg * dg;
+  // L_Y = L~ D^{-1/2}, D_Y = diag(L~)^2 out: row-owning threads, 8 pivot columns per batch of loads
+  __syncthreads();
+  double* __restrict__ Lp = a.Lp + a.panel_off[r];
+  for (int ar = tid; ar < c; ar += NT) {
+    for (int t0 = 0; t0 < s; t0 += 8) {
+      double dgv[8], fv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t0 + u < s) {
+          dgv[u] = F[(t0 + u) + (size_t)(t0 + u) * c];
+          fv[u] = F[ar + (size_t)(t0 + u) * c];
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (t0 + u < s) {
+          const int t = t0 + u;
+          const double rdg = 1.0 / dgv[u];
+          Lp[ar + (size_t)t * c] = ar > t ? fv[u] * rdg : (ar == t ? 1.0 : 0.0);
+        }
+    }
+  }
+  for (int t = tid; t < s; t += NT) {
+    const double dg = F[t + (size_t)t * c];
+    a.D[f + t] = dg * dg;
   }
 }
 
@@ -591,14 +638,26 @@ __global__ void __launch_bounds__(256) big_backsub_kernel(CliqueArgs a, const in
   Scratch sc{inv, l11, nullptr, &flag};
   cta_backsub_last_rows<256>(A, W, c, s, sc, ld);
   const int tid = threadIdx.x;
-  double* Lp = a.Lp + a.panel_off[r];
-  for (int idx = tid; idx < c * s; idx += 256) {
-    const int ar = idx % c, t = idx / c;
-    const double dg = W[(c - 1 - t) + (size_t)(s - 1 - t) * c];
-    double v;
-    if (ar > t) v = W[(c - 1 - ar) + (size_t)(s - 1 - t) * c] / dg;
-    else v = (ar == t) ? 1.0 : 0.0;
-    Lp[idx] = v;
+  double* __restrict__ Lp = a.Lp + a.panel_off[r];
+  for (int idx0 = tid; idx0 < c * s; idx0 += 256 * 4) {  // 4 elements per batch of (global) loads
+    double dg[4], wv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = idx0 + e * 256;
+      if (idx < c * s) {
+        const int ar = idx % c, t = idx / c;
+        dg[e] = W[(c - 1 - t) + (size_t)(s - 1 - t) * c];
+        wv[e] = W[(c - 1 - ar) + (size_t)(s - 1 - t) * c];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = idx0 + e * 256;
+      if (idx < c * s) {
+        const int ar = idx % c, t = idx / c;
+        Lp[idx] = ar > t ? wv[e] / dg[e] : (ar == t ? 1.0 : 0.0);
+      }
+    }
   }
   for (int t = tid; t < s; t += 256) {
     const double dg = W[(c - 1 - t) + (size_t)(s - 1 - t) * c];
@@ -842,9 +901,9 @@ int launch_ldl_y(sdpc_ctx* h, const double* y, cudaStream_t st, int32_t* err, in
     if (nbig > 0) {  // big fronts on the level's own stream, concurrent with the class kernels
       static std::atomic<uint64_t> attr{0};
       if (once_per_device(attr))
-        cudaFuncSetAttribute(front_panel_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(front_panel_kernel<kPanelNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (h->big_wide[lvi]) {
-        front_panel_kernel<256><<<nbig, 256, h->big_smem, st>>>(a, h->d_big_list + b0, (int)h->big_smem);
+        front_panel_kernel<kPanelNT><<<nbig, kPanelNT, h->big_smem, st>>>(a, h->d_big_list + b0, (int)h->big_smem);
         if (h->big_tiles[lvi] > 0)
           front_schur_kernel<<<dim3(h->big_tiles[lvi], nbig), 256, 0, st>>>(a, h->d_big_list + b0);
         n += 1 + (h->big_tiles[lvi] > 0);
