@@ -52,6 +52,7 @@ struct SolveArgs {
 };
 
 constexpr int kSolveThreads = 256;
+constexpr int kOcc3Panels = 592;           // >= two rounds of the 296 two-per-SM slots: use 3 CTAs per SM
 constexpr int kSolveSmemCap = 110 * 1024;  // opt-in of inverse_panel_kernel (2 CTAs per SM)
 
 __device__ __forceinline__ double& xrow(double* X, int row, int lane) { return X[(size_t)row * kPanelW + lane]; }
@@ -652,11 +653,20 @@ __device__ __forceinline__ void solve_panel(const SolveArgs& a, const int P, con
 }
 
 // One CTA per (RHS panel, factor); with gridDim.x < npanels (the X-hat solves that overlap the
-// tree-level (a2) launches leave SMs free for them) each CTA walks panels blockIdx.x + k gridDim.x.
-__global__ void __launch_bounds__(kSolveThreads, 2) inverse_panel_kernel(SolveArgs a) {
+// tree-level (a2) launches leave SMs free for them) each CTA walks one panel per round of gridDim.x.
+// MINB = 3 (80 registers, some spills) pays when the solve is CTA-wide DMMA sweeps over big supernodes
+// (block-arrow: (b) 25.2 -> 20.0 ms); on the deep trees of the tori, where per-warp walks over small
+// supernodes dominate, it is slower (configs[1] (b) done 5.8 -> 6.4 ms), so the launch picks.
+template <int MINB>
+__global__ void __launch_bounds__(kSolveThreads, MINB) inverse_panel_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double smem_solve[];
   const int fac = blockIdx.y + a.fac0;
-  for (int P = blockIdx.x; P < a.npanels; P += gridDim.x) {
+  // rounds of gridDim.x panels; odd rounds in reverse, so that the CTA with the most expensive panel of
+  // one round (low elimination indices: long reach, little truncated) takes the cheapest of the next
+  const int G = gridDim.x;
+  for (int k = 0; k * G < a.npanels; ++k) {
+    const int P = (k & 1) ? min((k + 1) * G, a.npanels) - 1 - (int)blockIdx.x : k * G + (int)blockIdx.x;
+    if (P < k * G || P >= a.npanels) break;
     solve_panel(a, P, fac, smem_solve);
     __syncthreads();
   }
@@ -713,13 +723,19 @@ static int launch_panels(sdpc_ctx* h, cudaStream_t st, int fac0, int nfac, int m
   }
   const size_t smem = solve_smem_bytes(h->S.nsuper);
   static std::atomic<uint64_t> attr{0};
-  if (once_per_device(attr))
-    cudaFuncSetAttribute(inverse_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmemCap);
+  if (once_per_device(attr)) {
+    cudaFuncSetAttribute(inverse_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmemCap);
+    cudaFuncSetAttribute(inverse_panel_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSolveSmemCap);
+  }
   if (h->d.npanels == 0) return 0;
   a.fac0 = fac0;
   a.npanels = h->d.npanels;
   dim3 grid(max_ctas > 0 ? std::min(h->d.npanels, max_ctas) : h->d.npanels, nfac);
-  inverse_panel_kernel<<<grid, kSolveThreads, smem, st>>>(a);
+  // three CTAs per SM when three fit the SM's shared memory and the work is CTA-wide DMMA sweeps over big
+  // supernodes (shallow elimination trees: block-arrow) or the panels are many
+  const bool occ3 = (h->a2lev.size() < 8 || h->d.npanels >= kOcc3Panels) && 3 * (smem + 1024) <= (size_t)227 * 1024;
+  if (occ3) inverse_panel_kernel<3><<<grid, kSolveThreads, smem, st>>>(a);
+  else inverse_panel_kernel<2><<<grid, kSolveThreads, smem, st>>>(a);
   return 1;
 }
 
