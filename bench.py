@@ -46,8 +46,8 @@ FALLBACK_BF16 = dict(burst=1590.0, sustained=1400.0)   # B200_PROFILING.md fallb
 FALLBACK_HBM = 6650.0
 # ncu --set full of one chol_dag_kernel launch on a 10,000^2 SPD matrix (configs[1]'s m): dram__bytes_read.sum +
 # dram__bytes_write.sum per algorithmic flop (m^3/3), scaled to the step's m^3/3 (profiles/r02/ncu/).
-DAG_BYTES_PER_FLOP = (4.226713e9 + 4.040358e9) / (1e4 ** 3 / 3.0)
-DAG_TRAFFIC_SOURCE = ("profiles/r02/ncu/dag_c1_full.txt: 4.23 GB read + 4.04 GB written by one chol_dag_kernel launch "
+DAG_BYTES_PER_FLOP = (4.289942e9 + 4.113768e9) / (1e4 ** 3 / 3.0)
+DAG_TRAFFIC_SOURCE = ("profiles/r02/final3/ncu_dag_full.txt: 4.29 GB read + 4.11 GB written by one chol_dag_kernel launch "
                       "at m = 10,000 (3.33e11 flops), scaled by the step's m^3/3")
 
 
@@ -271,7 +271,7 @@ def run_ours(args, rank, world, local_rank):
                  "window overlaps (a2)); FP64 roof = the line's peak.  (c): B lower triangle written once "
                  "(8 m(m+1)/2 bytes) over the accumulate kernel; HBM roof = MEASURED_PEAKS hbm_gbs; "
                  "*_with_panel_reads adds the one read of the materialised truncated X-hat / Y^-1 panels the "
-                 "unfused kernel needs (ncu: profiles/r02/ncu/scm_c1_full.txt, 0.99 GB read + 0.45 GB written).  (d): m^3/3 "
+                 "unfused kernel needs (ncu: profiles/r02/final3/ncu_scm_trunc_full.txt, 0.84 GB read + 0.40 GB written).  (d): m^3/3 "
                  "over the Cholesky kernel."),
     }
     for key in ("b_solve_x", "b_solve_y", "d_cholesky"):
