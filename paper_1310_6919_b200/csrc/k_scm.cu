@@ -37,14 +37,13 @@ __global__ void __launch_bounds__(256) scm_maxcut_kernel(int n, int m, const dou
                                                          const double* __restrict__ aval,
                                                          const int32_t* __restrict__ col_cons, double* B,
                                                          int64_t ldb, Grid g) {
-  __shared__ int32_t lcol[kPanelW], lvtx[kPanelW];
+  __shared__ int32_t lcol[kPanelW];
   __shared__ double lval[kPanelW];
   const int P = blockIdx.y;
   if (threadIdx.x < kPanelW) {
     const int v = rhs[P * kPanelW + threadIdx.x];
     const int l = v >= 0 ? col_cons[v] : -1;
     lcol[threadIdx.x] = l;
-    lvtx[threadIdx.x] = v;
     lval[threadIdx.x] = l >= 0 ? aval[l] : 0.0;
   }
   __syncthreads();
@@ -134,9 +133,12 @@ __global__ void __launch_bounds__(256) scm_general_kernel(int n, int m, const do
   if (is_large[l] || !g.own_col(l)) return;
   const int64_t lb = ptr[l];
   const int nl = (int)(ptr[l + 1] - lb);
+  // the RHS slots of A_l's columns are looked up once per CTA (sp / sq hold the element offset of the
+  // slot's panel column, so a gather is one dependent load, not two)
   for (int t = threadIdx.x; t < nl; t += blockDim.x) {
-    sp[t] = ei[lb + t];
-    sq[t] = ej[lb + t];
+    const int s0 = slot_of[ei[lb + t]], s1 = slot_of[ej[lb + t]];
+    sp[t] = s0;
+    sq[t] = s1;
     sw[t] = ev[lb + t];
   }
   __syncthreads();
@@ -147,8 +149,11 @@ __global__ void __launch_bounds__(256) scm_general_kernel(int n, int m, const do
     for (int64_t e = ptr[k]; e < ptr[k + 1]; ++e) {
       const int i = ei[e], j = ej[e];
       const double v = ev[e];
-      for (int t = 0; t < nl; ++t)
-        sum += v * sw[t] * pm(Xh, slot_of, n, j, sp[t]) * pm(Yh, slot_of, n, i, sq[t]);
+      for (int t = 0; t < nl; ++t) {
+        const int s0 = sp[t], s1 = sq[t];
+        sum += v * sw[t] * Xh[((size_t)(s0 >> 5) * n + j) * kPanelW + (s0 & 31)] *
+               Yh[((size_t)(s1 >> 5) * n + i) * kPanelW + (s1 & 31)];
+      }
     }
     Bl[g.lrow(k)] = sum;
   }

@@ -238,7 +238,7 @@ def _sampled(inst, seed=1, nsample=1000):
 
 @pytest.mark.parametrize("cfg", [1, 3, 4, 5])
 def test_full_config_sampled_columns(cfg):
-    """configs[1], [3], [4] at full size: >= 1000 sampled columns of B, plus free checks."""
+    """configs[1], [3], [4], [5] at full size: both factors, >= 1000 sampled columns of B, plus free checks."""
     from instances import gen_config
     inst = gen_config(cfg)
     S = SYM.analyse(inst.n, inst.perm, inst.a_row, inst.a_col)
@@ -248,6 +248,9 @@ def test_full_config_sampled_columns(cfg):
     assert np.array_equal(st["super_ptr"], S.super_ptr)
     L, D = A1.factor_xinv(S, inst.xbar)
     assert rel(g["L"], L) < 1e-11 and rel(g["D"], D) < 1e-11
+    # (a2) at full size: the multifrontal factor of Y against the oracle's up-looking LDL^T on E
+    Ly, Dy = LDL.ldl_on_E(S, inst.y)
+    assert rel(g["Ly"], Ly) < 1e-11 and rel(g["Dy"], Dy) < 1e-11
     cols = _sampled(inst)
     solver = SCM.ColumnSolver(S, L, D, inst.y, inst.perm)
     Bo = SCM.scm_columns(inst, cols, solver)
